@@ -1,0 +1,150 @@
+/*
+ * ocp_gpu.h - C ABI of the B200 (sm_100a) RASPEN hot path.
+ *
+ * The reference (`ocp`, pure Python) has no FFI; its operator protocol for
+ * this path is a set of Python callables.  These entry points
+ * are what a binding of that protocol needs; each cites the reference
+ * function it replaces.  Conventions:
+ *
+ *   - plain pointers and sizes only; "dev" pointers are CUDA device memory
+ *     (from ocp_malloc), "host" pointers are ordinary host memory;
+ *   - every call returns an ocp_status; no exception crosses the ABI;
+ *     ocp_last_error(ctx) holds the message of the last failing call;
+ *   - one context per (problem, decomposition); one CUDA stream per context;
+ *     calls on one context are not reentrant (the Python shim serialises);
+ *   - global vectors are [y; p] of length 2N, N = n*n, row-major fields
+ *     (`pkg/src/ocp/system.py:109-115`, `pkg/src/ocp/grid.py:26-33`);
+ *   - "reference local layout" is [y_loc; p_loc] with the overlap rectangle
+ *     row-major, concatenated over subdomains in decomposition order
+ *     (`pkg/src/ocp/schwarz.py:88-91,116-119`).
+ */
+#ifndef OCP_GPU_H
+#define OCP_GPU_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ocp_ctx ocp_ctx;
+
+typedef enum {
+  OCP_OK = 0,
+  OCP_ERR_ARG = 1,            /* ValueError: bad argument / decomposition */
+  OCP_ERR_CUDA = 2,           /* CUDA runtime failure */
+  OCP_ERR_LOCAL_SOLVE = 3,    /* LocalSolveError(subdomain, msg), schwarz.py:32-37 */
+  OCP_ERR_NONFINITE = 4,      /* NonfiniteFieldError(where, index), grid.py:9-23 */
+  OCP_ERR_NONFINITE_INIT = 5, /* ValueError("nonfinite residual at the initial guess"), newton.py:146-147 */
+  OCP_ERR_UNSUPPORTED = 6,    /* shape outside the compiled kernel limits */
+  OCP_ERR_NO_DEVICE = 7
+} ocp_status;
+
+/* phi selector: kappa*(s^3+e^{kappa s}) (system.py:31-74), y^3, e^y-1 */
+enum { OCP_PHI_KAPPA = 0, OCP_PHI_CUBIC = 1, OCP_PHI_EXPM1 = 2 };
+
+/* ---- context ------------------------------------------------------------
+ * Replaces decompose + build_local_systems (schwarz.py:94-163): builds the
+ * reference tiling (_tile_edges: remainder to the last tile, overlap clipped),
+ * uploads f and y_d, sizes the local pools.  Errors mirror decompose's
+ * ValueErrors (message in ocp_last_error(NULL) when *out is not created). */
+int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu,
+                   int phi_kind, double kappa, const double* f_host,
+                   const double* y_d_host, ocp_ctx** out);
+void ocp_ctx_destroy(ocp_ctx* ctx);
+const char* ocp_last_error(const ocp_ctx* ctx);
+/* info[0]=subdomains, [1]=local pool doubles, [2]=factor-store doubles,
+ * [3]=max padded half-bandwidth, [4]=panel width NB, [5]=sum of 2*R_i*C_i,
+ * [6]=reference-layout local length */
+int ocp_ctx_info(const ocp_ctx* ctx, long long* info);
+/* rects[11*i ...]: r0 r1 c0 c1 own_r0 own_r1 own_c0 own_c1 orient nr nc */
+int ocp_subdomain_table(const ocp_ctx* ctx, int* rects);
+
+/* ---- device memory (the context's stream) ------------------------------ */
+int ocp_malloc(size_t bytes, void** dev);
+int ocp_free(void* dev);
+int ocp_h2d(ocp_ctx* ctx, void* dev, const void* host, size_t bytes);
+int ocp_d2h(ocp_ctx* ctx, void* host, const void* dev, size_t bytes);
+int ocp_d2d(ocp_ctx* ctx, void* dst, const void* src, size_t bytes);
+int ocp_memset0(ocp_ctx* ctx, void* dev, size_t bytes);
+int ocp_sync(ocp_ctx* ctx);
+
+/* ---- the hot path ------------------------------------------------------- */
+
+/* One RAS sweep: every subdomain's frozen-exterior damped Newton with the
+ * eps schedule (eps0, gamma, eps_min) [inner newton_continuation,
+ * newton.py:133-181, via _solve_local schwarz.py:194-200], then the
+ * refactorisation at the converged values into fac_dev (schwarz.py:305-315)
+ * and f_val = sum_i P~_i values_i - x (schwarz.py:317).
+ * Replaces raspen_residual (schwarz.py:285-324).
+ *   x_dev      [2N] frozen global iterate
+ *   fac_dev    factor store of ocp_ctx_info()[2] doubles (written)
+ *   fval_dev   [2N] output
+ *   inner_iters_host [I] per-subdomain inner Newton iterations
+ *   failed_sub_host  lowest failing subdomain or -1
+ * Returns OCP_ERR_LOCAL_SOLVE with the reference message text in
+ * ocp_last_error when a subdomain fails. */
+int ocp_raspen_residual(ocp_ctx* ctx, const double* x_dev, double* fac_dev,
+                        double eps0, double gamma, double eps_min,
+                        double inner_tol, int inner_max_outer, double sigma,
+                        int max_halvings, double* fval_dev,
+                        int* inner_iters_host, int* failed_sub_host);
+
+/* Jacobian action from the stored factors of the last ocp_raspen_residual
+ * into fac_dev: out[own_i] = -(d_loc + J_i^{-1} A_ext d)[own_i].
+ * Replaces raspen_jacobian_apply (schwarz.py:327-345). */
+int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac_dev, const double* d_dev,
+                   double* out_dev);
+
+/* Current local values (last sweep) in the reference local layout. */
+int ocp_local_values(ocp_ctx* ctx, double* values_dev);
+
+/* Parity hooks for the kernels: local residual of every subdomain at local
+ * values v (reference layout) with the exterior frozen at x
+ * (_local_problem.local_residual, schwarz.py:181-186), and one Newton
+ * direction -J(v)^{-1} F(v) by the batched banded LU (newton.py:127). */
+int ocp_local_residual(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
+                       double eps, double* r_ref_dev);
+int ocp_local_direction(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
+                        double eps, double* d_ref_dev);
+
+/* ---- GMRES vector kernels (krylov.py:44-151), deterministic reductions -- */
+int ocp_vec_nrm2(ocp_ctx* ctx, long long n, const double* x, double* out_host);
+int ocp_vec_dot(ocp_ctx* ctx, long long n, const double* x, const double* y,
+                double* out_host);
+/* out = x + alpha*d  (numpy: x + alpha * d, product rounded first) */
+int ocp_vec_add_scaled(ocp_ctx* ctx, long long n, const double* x, double alpha,
+                       const double* d, double* out);
+/* out = a*x  */
+int ocp_vec_scale(ocp_ctx* ctx, long long n, double a, const double* x, double* out);
+/* out = x / s */
+int ocp_vec_div(ocp_ctx* ctx, long long n, const double* x, double s, double* out);
+int ocp_vec_equal(ocp_ctx* ctx, long long n, const double* x, const double* y,
+                  int* equal_host);
+int ocp_vec_all_finite(ocp_ctx* ctx, long long n, const double* x, int* finite_host);
+/* Modified Gram-Schmidt of w against Q[:, 0..j] (columns ldq apart):
+ * h_i = q_i.w ; w -= h_i q_i (krylov.py:113-115), then h[j+1] = ||w||.
+ * h_host receives j+2 values. */
+int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j,
+            double* w, double* h_host);
+/* out = x + Q[:, :k] @ y  (krylov.py:151) */
+int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k,
+                 const double* y_host, const double* x, double* out);
+/* u = -(p + mu P_eps(-p/mu))/nu  (system.py:173-174) */
+int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps,
+                        double* u);
+
+/* ---- instrumentation (bench.py) ----------------------------------------
+ * stats[0]=kernel launches, [1]=factor ms, [2]=factor launches,
+ * [3]=solve ms (stored-factor JVP solves), [4]=solve launches,
+ * [5]=factor flops, [6]=JVP-solve factor bytes, [7]=residual-sweep ms,
+ * [8]=DOF-updates, [9]=jvp ms, [10]=inner-solve ms, [11]=mgs ms
+ * Times need ocp_set_profiling(ctx, 1) (CUDA events on the context stream). */
+int ocp_set_profiling(ocp_ctx* ctx, int on);
+int ocp_stats(ocp_ctx* ctx, double* stats, int len);
+int ocp_reset_stats(ocp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCP_GPU_H */

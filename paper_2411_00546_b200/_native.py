@@ -1,0 +1,134 @@
+"""ctypes binding of ``libocpgpu.so`` (the C ABI in ``include/ocp_gpu.h``).
+
+There is no CPU fallback: importing the hot path without the built library,
+or calling it without a CUDA device, raises ``NativeUnavailable``.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libocpgpu.so")
+
+OCP_OK = 0
+OCP_ERR_ARG = 1
+OCP_ERR_CUDA = 2
+OCP_ERR_LOCAL_SOLVE = 3
+OCP_ERR_NONFINITE = 4
+OCP_ERR_NONFINITE_INIT = 5
+OCP_ERR_UNSUPPORTED = 6
+OCP_ERR_NO_DEVICE = 7
+
+_c_int_p = ctypes.POINTER(ctypes.c_int)
+_c_dbl_p = ctypes.POINTER(ctypes.c_double)
+_c_ll_p = ctypes.POINTER(ctypes.c_longlong)
+_vp = ctypes.c_void_p
+_ll = ctypes.c_longlong
+_d = ctypes.c_double
+_i = ctypes.c_int
+
+# name -> argtypes (all return int status unless listed in _RESTYPES)
+SIGNATURES = {
+    "ocp_ctx_create": [_i, _i, _i, _i, _d, _d, _i, _d, _vp, _vp, ctypes.POINTER(_vp)],
+    "ocp_ctx_destroy": [_vp],
+    "ocp_last_error": [_vp],
+    "ocp_ctx_info": [_vp, _c_ll_p],
+    "ocp_subdomain_table": [_vp, _c_int_p],
+    "ocp_malloc": [ctypes.c_size_t, ctypes.POINTER(_vp)],
+    "ocp_free": [_vp],
+    "ocp_h2d": [_vp, _vp, _vp, ctypes.c_size_t],
+    "ocp_d2h": [_vp, _vp, _vp, ctypes.c_size_t],
+    "ocp_d2d": [_vp, _vp, _vp, ctypes.c_size_t],
+    "ocp_memset0": [_vp, _vp, ctypes.c_size_t],
+    "ocp_sync": [_vp],
+    "ocp_raspen_residual": [_vp, _vp, _vp, _d, _d, _d, _d, _i, _d, _i, _vp, _c_int_p, _c_int_p],
+    "ocp_raspen_jvp": [_vp, _vp, _vp, _vp],
+    "ocp_local_values": [_vp, _vp],
+    "ocp_local_residual": [_vp, _vp, _vp, _d, _vp],
+    "ocp_local_direction": [_vp, _vp, _vp, _d, _vp],
+    "ocp_vec_nrm2": [_vp, _ll, _vp, _c_dbl_p],
+    "ocp_vec_dot": [_vp, _ll, _vp, _vp, _c_dbl_p],
+    "ocp_vec_add_scaled": [_vp, _ll, _vp, _d, _vp, _vp],
+    "ocp_vec_scale": [_vp, _ll, _d, _vp, _vp],
+    "ocp_vec_div": [_vp, _ll, _vp, _d, _vp],
+    "ocp_vec_equal": [_vp, _ll, _vp, _vp, _c_int_p],
+    "ocp_vec_all_finite": [_vp, _ll, _vp, _c_int_p],
+    "ocp_mgs": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
+    "ocp_gemv_add": [_vp, _ll, _vp, _ll, _i, _c_dbl_p, _vp, _vp],
+    "ocp_recover_control": [_vp, _ll, _vp, _d, _vp],
+    "ocp_set_profiling": [_vp, _i],
+    "ocp_stats": [_vp, _c_dbl_p, _i],
+    "ocp_reset_stats": [_vp],
+}
+_RESTYPES = {"ocp_ctx_destroy": None, "ocp_last_error": ctypes.c_char_p}
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library is missing or no device is visible (no fallback exists)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code, message, where=""):
+        self.code = code
+        self.message = message
+        super().__init__(f"{where}: [{code}] {message}" if where else f"[{code}] {message}")
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path=LIB_PATH):
+    """Load and type the library (does not touch the GPU)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise NativeUnavailable(
+                f"{path} not built; run __graft_entry__.build() (nvcc, sm_100a)")
+        lib = ctypes.CDLL(path)
+        for name, args in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RESTYPES.get(name, ctypes.c_int)
+        _lib = lib
+        return lib
+
+
+def last_error(ctx=None):
+    msg = load().ocp_last_error(ctx)
+    return msg.decode() if msg else ""
+
+
+def check(rc, ctx=None, where=""):
+    if rc != OCP_OK:
+        raise NativeError(rc, last_error(ctx), where)
+
+
+def ptr(a):
+    """Host pointer of a C-contiguous float64/int array."""
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class DeviceBuffer:
+    """Raw device allocation owned by Python (freed on collection)."""
+
+    __slots__ = ("addr", "nbytes", "__weakref__")
+
+    def __init__(self, nbytes):
+        lib = load()
+        p = ctypes.c_void_p()
+        rc = lib.ocp_malloc(ctypes.c_size_t(max(int(nbytes), 16)), ctypes.byref(p))
+        if rc != OCP_OK:
+            raise NativeError(rc, last_error(), "ocp_malloc")
+        self.addr = p.value
+        self.nbytes = int(nbytes)
+
+    def __del__(self):
+        if getattr(self, "addr", None) and _lib is not None:
+            _lib.ocp_free(ctypes.c_void_p(self.addr))
+            self.addr = None

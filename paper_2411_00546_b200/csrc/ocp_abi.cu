@@ -1,0 +1,850 @@
+// C ABI + host driver of the RASPEN hot path (declared in include/ocp_gpu.h).
+//
+// The batched inner Newton below is Algorithm 1 (newton.py:133-181) run for
+// all subdomains at once with per-subdomain state (active / converged /
+// failed, iteration count, frozen threshold, line-search alpha).  All
+// decisions are made here on the host from device-reduced norms, in double,
+// with the reference's exact comparisons; only vectors live on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ocp_gpu.h"
+#include "ocp_kernels.cuh"
+
+using namespace ocp;
+
+namespace {
+
+thread_local std::string g_global_err;
+
+struct Event {
+  cudaEvent_t a, b;
+  int cls;
+  double flops, bytes;
+};
+
+enum { CLS_FACTOR = 0, CLS_SOLVE = 1, CLS_SWEEP = 2, CLS_JVP = 3, CLS_INNER_SOLVE = 4, CLS_MGS = 5 };
+
+}  // namespace
+
+struct ocp_ctx {
+  int n = 0, s1 = 0, s2 = 0, m = 0, I = 0;
+  long long N = 0;
+  Phys P{};
+  std::vector<SubInfo> subs;
+  std::vector<double> sub_flops;    // algorithmic band-LU flops per subdomain
+  std::vector<double> sub_fbytes;   // algorithmic factor bytes per subdomain
+  std::vector<long long> sub_dofs;  // 2 R C
+  SubInfo* d_subs = nullptr;
+  long long pool_len = 0, fac_len = 0, ref_len = 0, dof_total = 0;
+  int maxW = 0, maxNP = 0, maxWS = 0;
+  double *d_f = nullptr, *d_yd = nullptr;
+  double *V = nullptr, *R = nullptr, *D = nullptr, *B = nullptr, *JD = nullptr;
+  int *d_list_all = nullptr, *d_list = nullptr, *d_status = nullptr, *d_flags = nullptr;
+  double *d_alpha = nullptr, *d_norm2 = nullptr;
+  long long* d_bad = nullptr;
+  double* scratch = nullptr;
+  long long ws_stride = 0;
+  int lu_grid = 1, num_sms = 148;
+  double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
+  unsigned int* red_counter = nullptr;
+  int h_cap = 0;
+  cudaStream_t stream = nullptr;
+  // pinned host staging
+  double* h_norm2 = nullptr;
+  int* h_status = nullptr;
+  long long* h_bad = nullptr;
+  int* h_list = nullptr;
+  double* h_alpha = nullptr;
+  double* h_small = nullptr;
+  int* h_flags = nullptr;
+  std::string err;
+  // instrumentation
+  bool prof = false;
+  long long launches = 0;
+  std::vector<Event> pending;
+  std::vector<cudaEvent_t> free_events;
+  double stat_ms[6] = {0, 0, 0, 0, 0, 0};
+  double stat_cnt[6] = {0, 0, 0, 0, 0, 0};
+  double stat_flops = 0, stat_bytes = 0, stat_dof = 0;
+};
+
+namespace {
+
+int fail(ocp_ctx* ctx, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (ctx) ctx->err = buf; else g_global_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, OCP_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+#define CKL()                                                                      \
+  do {                                                                             \
+    ++ctx->launches;                                                               \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, OCP_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                             \
+  } while (0)
+
+cudaEvent_t get_event(ocp_ctx* ctx) {
+  if (!ctx->free_events.empty()) {
+    cudaEvent_t e = ctx->free_events.back();
+    ctx->free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct Timer {
+  ocp_ctx* ctx;
+  Event ev{};
+  bool on;
+  Timer(ocp_ctx* c, int cls, double flops = 0, double bytes = 0) : ctx(c), on(c->prof) {
+    if (!on) return;
+    ev.a = get_event(ctx);
+    ev.b = get_event(ctx);
+    ev.cls = cls;
+    ev.flops = flops;
+    ev.bytes = bytes;
+    cudaEventRecord(ev.a, ctx->stream);
+  }
+  ~Timer() {
+    if (!on) return;
+    cudaEventRecord(ev.b, ctx->stream);
+    ctx->pending.push_back(ev);
+  }
+};
+
+void drain_events(ocp_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    ctx->stat_ms[e.cls] += ms;
+    ctx->stat_cnt[e.cls] += 1;
+    if (e.cls == CLS_FACTOR) ctx->stat_flops += e.flops;
+    if (e.cls == CLS_SOLVE) ctx->stat_bytes += e.bytes;
+    ctx->free_events.push_back(e.a);
+    ctx->free_events.push_back(e.b);
+  }
+  ctx->pending.clear();
+}
+
+std::vector<std::pair<int, int>> tile_edges(int n, int parts, bool& ok) {
+  std::vector<std::pair<int, int>> out;
+  const int base = n / parts, rem = n % parts;
+  ok = base > 0;
+  if (!ok) return out;
+  for (int k = 0; k < parts; ++k) out.push_back({k * base, k * base + base + (k == parts - 1 ? rem : 0)});
+  return out;
+}
+
+// exact band-LU flop count: sum_k m_k (1 + 2 u_k), m_k = u_k = min(w, N-1-k)
+double band_lu_flops(long long N, long long w) {
+  double tot = 0.0;
+  for (long long k = 0; k < N; ++k) {
+    const double m = (double)std::min(w, N - 1 - k);
+    tot += m * (1.0 + 2.0 * m);
+  }
+  return tot;
+}
+
+int lu_smem_bytes(int W) { return (NB * (NB + W + 1) + NB * W) * (int)sizeof(double); }
+
+int upload_list(ocp_ctx* ctx, const std::vector<int>& list) {
+  std::copy(list.begin(), list.end(), ctx->h_list);
+  CK(cudaMemcpyAsync(ctx->d_list, ctx->h_list, list.size() * sizeof(int), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  return OCP_OK;
+}
+
+int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, double* fac) {
+  const int cnt = (int)list.size();
+  if (cnt == 0) return OCP_OK;
+  double flops = 0;
+  for (int i : list) flops += ctx->sub_flops[i];
+  Timer t(ctx, CLS_FACTOR, flops);
+  const int grid = std::min(cnt, ctx->lu_grid);
+  k_band_factor<<<grid, LU_THREADS, lu_smem_bytes(ctx->maxW), ctx->stream>>>(
+      ctx->d_subs, d_list, cnt, ctx->P, ctx->JD, fac, ctx->scratch, ctx->ws_stride, ctx->d_status);
+  CKL();
+  return OCP_OK;
+}
+
+int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, const double* fac,
+                 const double* in, double scale, double* out, int cls) {
+  const int cnt = (int)list.size();
+  if (cnt == 0) return OCP_OK;
+  double bytes = 0;
+  for (int i : list) bytes += ctx->sub_fbytes[i];
+  Timer t(ctx, cls, 0, bytes);
+  k_band_solve<<<cnt, 256, ctx->maxNP * sizeof(double), ctx->stream>>>(ctx->d_subs, d_list, fac, in,
+                                                                       scale, out);
+  CKL();
+  return OCP_OK;
+}
+
+inline int ew_grid(long long n) {
+  long long g = (n + 255) / 256;
+  return (int)std::max(1LL, std::min<long long>(g, 148LL * 16));
+}
+
+std::string fmt_e3(double v) {
+  char buf[64];
+  snprintf(buf, sizeof buf, "%.3e", v);
+  return buf;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ocp_last_error(const ocp_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_global_err.c_str();
+}
+
+int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int phi_kind,
+                   double kappa, const double* f_host, const double* y_d_host, ocp_ctx** out) {
+  ocp_ctx* ctx = nullptr;
+  if (!out) return fail(nullptr, OCP_ERR_ARG, "null output pointer");
+  *out = nullptr;
+  if (n < 1) return fail(nullptr, OCP_ERR_ARG, "grid needs at least one interior point per dimension");
+  if (s1 < 1 || s2 < 1) return fail(nullptr, OCP_ERR_ARG, "need at least one tile per dimension");
+  if (overlap < 0) return fail(nullptr, OCP_ERR_ARG, "overlap must be nonnegative");
+  if (!(nu > 0.0) || !(mu > 0.0)) return fail(nullptr, OCP_ERR_ARG, "nu and mu must be positive");
+  if (phi_kind < 0 || phi_kind > 2) return fail(nullptr, OCP_ERR_ARG, "unknown phi kind %d", phi_kind);
+  bool ok1, ok2;
+  auto rt = tile_edges(n, s1, ok1);
+  if (!ok1) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s1);
+  auto ct = tile_edges(n, s2, ok2);
+  if (!ok2) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s2);
+  auto minw = [](const std::vector<std::pair<int, int>>& t) {
+    int m = INT_MAX;
+    for (auto& e : t) m = std::min(m, e.second - e.first);
+    return m;
+  };
+  if (s1 > 1 && overlap > minw(rt))
+    return fail(nullptr, OCP_ERR_ARG, "overlap exceeds neighbor tile in the row direction");
+  if (s2 > 1 && overlap > minw(ct))
+    return fail(nullptr, OCP_ERR_ARG, "overlap exceeds neighbor tile in the column direction");
+  int dev_count = 0;
+  if (cudaGetDeviceCount(&dev_count) != cudaSuccess || dev_count == 0)
+    return fail(nullptr, OCP_ERR_NO_DEVICE, "no CUDA device visible");
+
+  ctx = new ocp_ctx();
+  ctx->n = n; ctx->s1 = s1; ctx->s2 = s2; ctx->m = overlap;
+  ctx->N = (long long)n * n;
+  const double h = 1.0 / (n + 1);
+  const double h2 = h * h;  // Python h ** 2 (correctly rounded square)
+  ctx->P.n = n;
+  ctx->P.phi_kind = phi_kind;
+  ctx->P.diag = 4.0 / h2;
+  ctx->P.off = -1.0 / h2;
+  ctx->P.nu = nu;
+  ctx->P.mu = mu;
+  ctx->P.kappa = kappa;
+  ctx->P.kappa2 = kappa * kappa;
+  long long loc = 0, fac = 0, ref = 0;
+  for (auto& r : rt) {
+    for (auto& c : ct) {
+      SubInfo s{};
+      s.r0 = std::max(0, r.first - overlap);
+      s.r1 = std::min(n, r.second + overlap);
+      s.c0 = std::max(0, c.first - overlap);
+      s.c1 = std::min(n, c.second + overlap);
+      s.or0 = r.first; s.or1 = r.second; s.oc0 = c.first; s.oc1 = c.second;
+      const int R = s.r1 - s.r0, C = s.c1 - s.c0;
+      s.orient = C <= R ? 0 : 1;
+      s.nr = std::max(R, C);
+      s.nc = std::min(R, C);
+      s.w = 2 * s.nc;
+      s.W = ((s.w + NB - 1) / NB) * NB;
+      s.N = 2 * R * C;
+      s.NP = ((s.N + NB - 1) / NB) * NB;
+      s.loc = loc;
+      s.fac = fac;
+      s.ref = ref;
+      loc += s.NP;
+      fac += (long long)s.NP * (2 * s.W + 1);
+      ref += s.N;
+      ctx->subs.push_back(s);
+      ctx->sub_flops.push_back(band_lu_flops(s.N, s.w));
+      ctx->sub_fbytes.push_back(8.0 * (double)s.N * (2.0 * s.w + 1.0));
+      ctx->sub_dofs.push_back(s.N);
+      ctx->maxW = std::max(ctx->maxW, s.W);
+      ctx->maxNP = std::max(ctx->maxNP, s.NP);
+    }
+  }
+  ctx->I = (int)ctx->subs.size();
+  ctx->pool_len = loc;
+  ctx->fac_len = fac;
+  ctx->ref_len = ref;
+  ctx->maxWS = ctx->maxW + NB;
+  if (ctx->maxW > MAX_W) {
+    int code = fail(nullptr, OCP_ERR_UNSUPPORTED,
+                    "local half-bandwidth %d exceeds the compiled limit %d", ctx->maxW, MAX_W);
+    delete ctx;
+    return code;
+  }
+  if ((long long)ctx->maxNP * 8 > 227 * 1024) {
+    int code = fail(nullptr, OCP_ERR_UNSUPPORTED, "local system of %d unknowns exceeds shared memory",
+                    ctx->maxNP);
+    delete ctx;
+    return code;
+  }
+  auto cleanup_fail = [&](int code) {
+    g_global_err = ctx->err;
+    ocp_ctx_destroy(ctx);
+    return code;
+  };
+#define CKC(call)                                                                       \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      fail(ctx, OCP_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));                \
+      return cleanup_fail(OCP_ERR_CUDA);                                                \
+    }                                                                                   \
+  } while (0)
+  int dev = 0;
+  CKC(cudaGetDevice(&dev));
+  CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  const int I = ctx->I;
+  CKC(cudaMalloc(&ctx->d_subs, I * sizeof(SubInfo)));
+  CKC(cudaMemcpy(ctx->d_subs, ctx->subs.data(), I * sizeof(SubInfo), cudaMemcpyHostToDevice));
+  const size_t nbytes = ctx->N * sizeof(double);
+  CKC(cudaMalloc(&ctx->d_f, nbytes));
+  CKC(cudaMalloc(&ctx->d_yd, nbytes));
+  CKC(cudaMemcpy(ctx->d_f, f_host, nbytes, cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(ctx->d_yd, y_d_host, nbytes, cudaMemcpyHostToDevice));
+  const size_t pbytes = ctx->pool_len * sizeof(double);
+  for (double** p : {&ctx->V, &ctx->R, &ctx->D, &ctx->B}) {
+    CKC(cudaMalloc(p, pbytes));
+    CKC(cudaMemset(*p, 0, pbytes));
+  }
+  CKC(cudaMalloc(&ctx->JD, 2 * pbytes));
+  CKC(cudaMemset(ctx->JD, 0, 2 * pbytes));
+  CKC(cudaMalloc(&ctx->d_list_all, I * sizeof(int)));
+  CKC(cudaMalloc(&ctx->d_list, I * sizeof(int)));
+  CKC(cudaMalloc(&ctx->d_status, I * sizeof(int)));
+  CKC(cudaMalloc(&ctx->d_alpha, I * sizeof(double)));
+  CKC(cudaMalloc(&ctx->d_norm2, I * sizeof(double)));
+  CKC(cudaMalloc(&ctx->d_bad, I * sizeof(long long)));
+  CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(int)));
+  {
+    std::vector<int> all(I);
+    for (int i = 0; i < I; ++i) all[i] = i;
+    CKC(cudaMemcpy(ctx->d_list_all, all.data(), I * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  // LU windows: up to 2 CTAs per SM, one (W+NB)^2 window each (L2 resident)
+  ctx->lu_grid = std::min(I, 2 * ctx->num_sms);
+  ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
+  CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
+  CKC(cudaMalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
+  CKC(cudaMalloc(&ctx->red_counter, sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->red_counter, 0, sizeof(unsigned int)));
+  CKC(cudaMalloc(&ctx->d_result, 8 * sizeof(double)));
+  ctx->h_cap = 4096;
+  CKC(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_norm2, I * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_status, I * sizeof(int)));
+  CKC(cudaMallocHost(&ctx->h_bad, I * sizeof(long long)));
+  CKC(cudaMallocHost(&ctx->h_list, I * sizeof(int)));
+  CKC(cudaMallocHost(&ctx->h_alpha, I * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_small, 8192 * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_flags, 4 * sizeof(int)));
+  CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           lu_smem_bytes(MAX_W)));
+  CKC(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024));
+#undef CKC
+  for (auto& s : ctx->subs) ctx->dof_total += s.N;
+  *out = ctx;
+  return OCP_OK;
+}
+
+void ocp_ctx_destroy(ocp_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
+                  (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
+                  (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_flags, (void*)ctx->scratch,
+                  (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
+                  (void*)ctx->d_h})
+    if (p) cudaFree(p);
+  for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
+                  (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags})
+    if (p) cudaFreeHost(p);
+  for (auto& e : ctx->pending) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : ctx->free_events) cudaEventDestroy(e);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int ocp_ctx_info(const ocp_ctx* ctx, long long* info) {
+  if (!ctx || !info) return OCP_ERR_ARG;
+  info[0] = ctx->I;
+  info[1] = ctx->pool_len;
+  info[2] = ctx->fac_len;
+  info[3] = ctx->maxW;
+  info[4] = NB;
+  info[5] = ctx->dof_total;
+  info[6] = ctx->ref_len;
+  return OCP_OK;
+}
+
+int ocp_subdomain_table(const ocp_ctx* ctx, int* rects) {
+  if (!ctx || !rects) return OCP_ERR_ARG;
+  for (int i = 0; i < ctx->I; ++i) {
+    const SubInfo& s = ctx->subs[i];
+    const int v[11] = {s.r0, s.r1, s.c0, s.c1, s.or0, s.or1, s.oc0, s.oc1, s.orient, s.nr, s.nc};
+    std::memcpy(rects + 11 * i, v, sizeof v);
+  }
+  return OCP_OK;
+}
+
+int ocp_malloc(size_t bytes, void** dev) {
+  ocp_ctx* ctx = nullptr;
+  if (!dev) return OCP_ERR_ARG;
+  CK(cudaMalloc(dev, std::max<size_t>(bytes, 16)));
+  return OCP_OK;
+}
+
+int ocp_free(void* dev) {
+  ocp_ctx* ctx = nullptr;
+  if (dev) CK(cudaFree(dev));
+  return OCP_OK;
+}
+
+int ocp_h2d(ocp_ctx* ctx, void* dev, const void* host, size_t bytes) {
+  CK(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_d2h(ocp_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  CK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_d2d(ocp_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_memset0(ocp_ctx* ctx, void* dev, size_t bytes) {
+  CK(cudaMemsetAsync(dev, 0, bytes, ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_sync(ocp_ctx* ctx) {
+  CK(cudaStreamSynchronize(ctx->stream));
+  return OCP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the RAS sweep (raspen_residual, schwarz.py:285-324)
+// ---------------------------------------------------------------------------
+int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0, double gamma,
+                        double eps_min, double tol, int max_outer, double sigma, int max_halvings,
+                        double* fval, int* inner_iters, int* failed_sub) {
+  if (!ctx || !x || !fac || !fval) return fail(ctx, OCP_ERR_ARG, "null argument");
+  const int I = ctx->I;
+  cudaStream_t st = ctx->stream;
+  Timer sweep_timer(ctx, CLS_SWEEP);
+  enum { ACTIVE = 0, DONE = 1, FAILED = 2 };
+  struct Failure {
+    int code;
+    std::string msg;
+  };
+  std::vector<int> state(I, ACTIVE), iters(I, 0);
+  std::vector<double> nrm(I), thr(I), alpha(I, 1.0);
+  std::vector<Failure> why(I);
+  int lowest = INT_MAX;
+  auto mark_fail = [&](int i, int code, const std::string& msg) {
+    state[i] = FAILED;
+    why[i] = {code, msg};
+    lowest = std::min(lowest, i);
+  };
+
+  k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->V);
+  CKL();
+  double eps = eps0;
+  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->V, nullptr, nullptr,
+                                ctx->d_f, ctx->d_yd, eps, ctx->R, ctx->d_norm2);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < I; ++i) {
+    nrm[i] = std::sqrt(ctx->h_norm2[i]);
+    if (!std::isfinite(nrm[i])) {
+      mark_fail(i, OCP_ERR_NONFINITE_INIT, "nonfinite residual at the initial guess");
+      continue;
+    }
+    thr[i] = std::max(tol, tol * nrm[i]);  // newton.py:148
+  }
+
+  std::vector<int> act, pend, acc, next;
+  while (true) {
+    act.clear();
+    for (int i = 0; i < I && i < lowest; ++i) {
+      if (state[i] != ACTIVE) continue;
+      if (nrm[i] <= thr[i] && eps == eps_min) {  // newton.py:153
+        state[i] = DONE;
+      } else if (iters[i] >= max_outer) {
+        char buf[128];
+        snprintf(buf, sizeof buf, "no convergence within %d outer iterations", max_outer);
+        mark_fail(i, OCP_ERR_LOCAL_SOLVE, buf);
+      } else {
+        act.push_back(i);
+      }
+    }
+    // subdomains above a known failure cannot change the outcome
+    act.erase(std::remove_if(act.begin(), act.end(), [&](int i) { return i > lowest; }), act.end());
+    if (act.empty()) break;
+    const int cnt = (int)act.size();
+    if (int rc = upload_list(ctx, act)) return rc;
+    k_jacdiag<<<cnt, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, ctx->V, eps, ctx->JD, ctx->d_bad);
+    CKL();
+    if (int rc = launch_factor(ctx, ctx->d_list, act, fac)) return rc;
+    if (int rc = launch_solve(ctx, ctx->d_list, act, fac, ctx->R, -1.0, ctx->D, CLS_INNER_SOLVE)) return rc;
+    CK(cudaMemcpyAsync(ctx->h_bad, ctx->d_bad, I * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    pend.clear();
+    for (int i : act) {
+      const long long b = ctx->h_bad[i];
+      if (b >= 0) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "%s@%lld", (b >> 32) ? "phi''(y)" : "phi'(y)", b & 0xffffffffLL);
+        mark_fail(i, OCP_ERR_NONFINITE, buf);
+      } else if (ctx->h_status[i]) {
+        mark_fail(i, OCP_ERR_LOCAL_SOLVE,
+                  "sparse factorization failed: singular local Jacobian (zero pivot in banded LU)");
+      } else {
+        pend.push_back(i);
+        alpha[i] = 1.0;
+      }
+    }
+    // relaxed backtracking (newton.py:96-112), all pending subdomains at once
+    acc.clear();
+    for (int h = 0; h <= max_halvings && !pend.empty(); ++h) {
+      for (size_t k = 0; k < pend.size(); ++k) ctx->h_alpha[pend[k]] = alpha[pend[k]];
+      CK(cudaMemcpyAsync(ctx->d_alpha, ctx->h_alpha, I * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (int rc = upload_list(ctx, pend)) return rc;
+      k_residual<<<(int)pend.size(), 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, x, ctx->V,
+                                                    ctx->D, ctx->d_alpha, ctx->d_f, ctx->d_yd, eps,
+                                                    nullptr, ctx->d_norm2);
+      CKL();
+      CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      next.clear();
+      for (int i : pend) {
+        const double trial = std::sqrt(ctx->h_norm2[i]);
+        if (std::isfinite(trial) && trial <= sigma * nrm[i]) acc.push_back(i);
+        else {
+          alpha[i] *= 0.5;
+          next.push_back(i);
+        }
+      }
+      pend.swap(next);
+    }
+    for (int i : pend) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "no admissible step within %d halvings (residual %s)", max_halvings,
+               fmt_e3(nrm[i]).c_str());
+      mark_fail(i, OCP_ERR_LOCAL_SOLVE, buf);
+    }
+    const double eps_next = (eps_min > gamma * eps) ? eps_min : gamma * eps;  // max(gamma*eps, eps_min)
+    if (!acc.empty()) {
+      std::sort(acc.begin(), acc.end());
+      for (int i : acc) ctx->h_alpha[i] = alpha[i];
+      CK(cudaMemcpyAsync(ctx->d_alpha, ctx->h_alpha, I * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (int rc = upload_list(ctx, acc)) return rc;
+      const int na = (int)acc.size();
+      k_update<<<na, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->V, ctx->D, ctx->d_alpha);
+      CKL();
+      k_residual<<<na, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, x, ctx->V, nullptr, nullptr,
+                                     ctx->d_f, ctx->d_yd, eps_next, ctx->R, ctx->d_norm2);
+      CKL();
+      CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int i : acc) {
+        nrm[i] = std::sqrt(ctx->h_norm2[i]);
+        iters[i] += 1;
+        ctx->stat_dof += (double)ctx->sub_dofs[i];
+      }
+    }
+    eps = eps_next;
+  }
+  if (inner_iters) for (int i = 0; i < I; ++i) inner_iters[i] = iters[i];
+  if (lowest != INT_MAX) {
+    if (failed_sub) *failed_sub = lowest;
+    return fail(ctx, why[lowest].code, "%s", why[lowest].msg.c_str());
+  }
+  if (failed_sub) *failed_sub = -1;
+  // refactorisation at the converged values (schwarz.py:305-315)
+  std::vector<int> all(I);
+  for (int i = 0; i < I; ++i) all[i] = i;
+  k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->V, eps_min, ctx->JD,
+                               ctx->d_bad);
+  CKL();
+  if (int rc = launch_factor(ctx, ctx->d_list_all, all, fac)) return rc;
+  {
+    dim3 grid(I, 8);
+    k_scatter_fval<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, ctx->V, x, fval);
+    CKL();
+  }
+  CK(cudaMemcpyAsync(ctx->h_bad, ctx->d_bad, I * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < I; ++i) {
+    if (ctx->h_bad[i] >= 0) {
+      const long long b = ctx->h_bad[i];
+      if (failed_sub) *failed_sub = i;
+      return fail(ctx, OCP_ERR_NONFINITE, "%s@%lld", (b >> 32) ? "phi''(y)" : "phi'(y)",
+                  b & 0xffffffffLL);
+    }
+    if (ctx->h_status[i]) {
+      if (failed_sub) *failed_sub = i;
+      return fail(ctx, OCP_ERR_LOCAL_SOLVE,
+                  "singular local Jacobian: zero pivot in banded LU");
+    }
+  }
+  return OCP_OK;
+}
+
+int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out) {
+  if (!ctx || !fac || !d || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  Timer t(ctx, CLS_JVP);
+  k_jvp_rhs<<<I, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B);
+  CKL();
+  std::vector<int> all(I);
+  for (int i = 0; i < I; ++i) all[i] = i;
+  if (int rc = launch_solve(ctx, ctx->d_list_all, all, fac, ctx->B, 1.0, ctx->B, CLS_SOLVE)) return rc;
+  dim3 grid(I, 8);
+  k_jvp_out<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B, out);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_local_values(ocp_ctx* ctx, double* values) {
+  k_band_to_ref<<<ctx->I, 256, 0, ctx->stream>>>(ctx->d_subs, ctx->V, values);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_local_residual(ocp_ctx* ctx, const double* x, const double* v_ref, double eps, double* r_ref) {
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
+  CKL();
+  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->B, nullptr, nullptr,
+                                ctx->d_f, ctx->d_yd, eps, ctx->D, ctx->d_norm2);
+  CKL();
+  k_band_to_ref<<<I, 256, 0, st>>>(ctx->d_subs, ctx->D, r_ref);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  return OCP_OK;
+}
+
+int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, double eps, double* d_ref) {
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  double* fac = nullptr;
+  CK(cudaMalloc(&fac, ctx->fac_len * sizeof(double)));
+  k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
+  CKL();
+  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->B, nullptr, nullptr,
+                                ctx->d_f, ctx->d_yd, eps, ctx->D, ctx->d_norm2);
+  CKL();
+  k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->B, eps, ctx->JD, ctx->d_bad);
+  CKL();
+  std::vector<int> all(I);
+  for (int i = 0; i < I; ++i) all[i] = i;
+  int rc = launch_factor(ctx, ctx->d_list_all, all, fac);
+  if (!rc) rc = launch_solve(ctx, ctx->d_list_all, all, fac, ctx->D, -1.0, ctx->D, CLS_INNER_SOLVE);
+  if (!rc) {
+    k_band_to_ref<<<I, 256, 0, st>>>(ctx->d_subs, ctx->D, d_ref);
+    CKL();
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(fac);
+  if (rc) return rc;
+  CK(cudaMemcpy(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < I; ++i)
+    if (ctx->h_status[i]) return fail(ctx, OCP_ERR_LOCAL_SOLVE, "zero pivot in subdomain %d", i);
+  return OCP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// vector kernels
+// ---------------------------------------------------------------------------
+int ocp_vec_dot(ocp_ctx* ctx, long long n, const double* x, const double* y, double* out) {
+  k_dot<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(n, x, y, ctx->red_partials, ctx->red_counter,
+                                                     ctx->d_result, 0);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_small, ctx->d_result, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = ctx->h_small[0];
+  return OCP_OK;
+}
+
+int ocp_vec_nrm2(ocp_ctx* ctx, long long n, const double* x, double* out) {
+  k_dot<<<RED_BLOCKS, RED_THREADS, 0, ctx->stream>>>(n, x, x, ctx->red_partials, ctx->red_counter,
+                                                     ctx->d_result, 1);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_small, ctx->d_result, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = ctx->h_small[0];
+  return OCP_OK;
+}
+
+int ocp_vec_add_scaled(ocp_ctx* ctx, long long n, const double* x, double alpha, const double* d,
+                       double* out) {
+  k_add_scaled<<<ew_grid(n), 256, 0, ctx->stream>>>(n, x, alpha, d, out);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_vec_scale(ocp_ctx* ctx, long long n, double a, const double* x, double* out) {
+  k_scale<<<ew_grid(n), 256, 0, ctx->stream>>>(n, a, x, out);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_vec_div(ocp_ctx* ctx, long long n, const double* x, double s, double* out) {
+  k_div<<<ew_grid(n), 256, 0, ctx->stream>>>(n, x, s, out);
+  CKL();
+  return OCP_OK;
+}
+
+static int run_flags(ocp_ctx* ctx, long long n, const double* x, const double* y, int* fl) {
+  ctx->h_flags[0] = 1;
+  ctx->h_flags[1] = 1;
+  CK(cudaMemcpyAsync(ctx->d_flags, ctx->h_flags, 2 * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  k_flags<<<ew_grid(n), 256, 0, ctx->stream>>>(n, x, y, ctx->d_flags);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_flags, ctx->d_flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  fl[0] = ctx->h_flags[0];
+  fl[1] = ctx->h_flags[1];
+  return OCP_OK;
+}
+
+int ocp_vec_equal(ocp_ctx* ctx, long long n, const double* x, const double* y, int* equal) {
+  int fl[2];
+  if (int rc = run_flags(ctx, n, x, y, fl)) return rc;
+  *equal = fl[0];
+  return OCP_OK;
+}
+
+int ocp_vec_all_finite(ocp_ctx* ctx, long long n, const double* x, int* finite) {
+  int fl[2];
+  if (int rc = run_flags(ctx, n, x, nullptr, fl)) return rc;
+  *finite = fl[1];
+  return OCP_OK;
+}
+
+int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j, double* w, double* h_host) {
+  if (j + 2 > ctx->h_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->d_h));
+    ctx->h_cap = 2 * (j + 2);
+    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+  }
+  Timer t(ctx, CLS_MGS);
+  cudaStream_t st = ctx->stream;
+  for (int i = 0; i <= j; ++i) {
+    k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, i > 0 ? Q + (long long)(i - 1) * ldq : nullptr,
+                                                   i > 0 ? ctx->d_h + i - 1 : nullptr,
+                                                   Q + (long long)i * ldq, ctx->red_partials,
+                                                   ctx->red_counter, ctx->d_h + i);
+    CKL();
+  }
+  k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, Q + (long long)j * ldq, ctx->d_h + j, nullptr,
+                                                 ctx->red_partials, ctx->red_counter, ctx->d_h + j + 1);
+  CKL();
+  CK(cudaMemcpyAsync(h_host, ctx->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return OCP_OK;
+}
+
+int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k, const double* y_host,
+                 const double* x, double* out) {
+  if (k + 2 > ctx->h_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->d_h));
+    ctx->h_cap = 2 * (k + 2);
+    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+  }
+  CK(cudaMemcpyAsync(ctx->d_h, y_host, k * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  k_gemv_add<<<ew_grid(n), 256, 0, ctx->stream>>>(n, Q, ldq, k, ctx->d_h, x, out);
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps, double* u) {
+  k_recover_control<<<ew_grid(n), 256, 0, ctx->stream>>>(n, ctx->P, p, eps, u);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_set_profiling(ocp_ctx* ctx, int on) {
+  if (!ctx) return OCP_ERR_ARG;
+  ctx->prof = on != 0;
+  return OCP_OK;
+}
+
+int ocp_stats(ocp_ctx* ctx, double* stats, int len) {
+  if (!ctx || !stats) return OCP_ERR_ARG;
+  drain_events(ctx);
+  double v[12] = {(double)ctx->launches, ctx->stat_ms[CLS_FACTOR], ctx->stat_cnt[CLS_FACTOR],
+                  ctx->stat_ms[CLS_SOLVE], ctx->stat_cnt[CLS_SOLVE], ctx->stat_flops,
+                  ctx->stat_bytes, ctx->stat_ms[CLS_SWEEP], ctx->stat_dof, ctx->stat_ms[CLS_JVP],
+                  ctx->stat_ms[CLS_INNER_SOLVE], ctx->stat_ms[CLS_MGS]};
+  for (int i = 0; i < len && i < 12; ++i) stats[i] = v[i];
+  return OCP_OK;
+}
+
+int ocp_reset_stats(ocp_ctx* ctx) {
+  if (!ctx) return OCP_ERR_ARG;
+  drain_events(ctx);
+  ctx->launches = 0;
+  for (int i = 0; i < 6; ++i) ctx->stat_ms[i] = ctx->stat_cnt[i] = 0;
+  ctx->stat_flops = ctx->stat_bytes = ctx->stat_dof = 0;
+  return OCP_OK;
+}
+
+}  // extern "C"

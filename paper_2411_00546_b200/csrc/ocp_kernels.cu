@@ -1,0 +1,419 @@
+// Pointwise / stencil / scatter kernels of the RASPEN hot path (sm_100a).
+//
+// Every value that feeds a Newton decision is computed with explicit
+// round-to-nearest operations in the reference's evaluation order
+// (system.py:118-144, schwarz.py:174-186, scipy CSR row order), so the local
+// residuals match the CPU oracle bitwise for the polynomial phi's.
+#include "ocp_kernels.cuh"
+
+namespace ocp {
+
+// ---------------------------------------------------------------------------
+// deterministic block reduction (fixed tree, fixed blockDim)
+// ---------------------------------------------------------------------------
+template <int THREADS>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < THREADS / 32 ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  }
+  __syncthreads();
+  return r;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------------------
+// local value of the (optionally line-searched) iterate: v + alpha*d
+// (newton.py:106: x + alpha * d, product rounded first)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 lval(const double2* V, const double2* D, double alpha, int q) {
+  double2 v = V[q];
+  if (D) {
+    const double2 d = D[q];
+    v.x = add(v.x, mul(alpha, d.x));
+    v.y = add(v.y, mul(alpha, d.y));
+  }
+  return v;
+}
+
+// 5-point stencil action on one local point with the exterior ring frozen at
+// the global iterate: (a_loc @ v)_q + (a_ext @ x)_q for both fields, each sum
+// in ascending global column order starting from 0.0 (csr_matvec), the two
+// parts added last (schwarz.py:183).
+__device__ __forceinline__ void stencil_point(const SubInfo& s, const Phys& P, const double2* V,
+                                              const double2* D, double alpha, const double* x,
+                                              long long Ntot, int i, int j, double& ay, double& ap) {
+  const int n = P.n;
+  double sly = 0.0, slp = 0.0, sey = 0.0, sep = 0.0;
+  const int di[5] = {-1, 0, 0, 0, 1};
+  const int dj[5] = {0, -1, 0, 1, 0};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int ii = i + di[t], jj = j + dj[t];
+    if (ii < 0 || ii >= n || jj < 0 || jj >= n) continue;
+    const double coef = (t == 2) ? P.diag : P.off;
+    if (in_rect(s, ii, jj)) {
+      const double2 v = lval(V, D, alpha, global_to_q(s, ii, jj));
+      sly = add(sly, mul(coef, v.x));
+      slp = add(slp, mul(coef, v.y));
+    } else {
+      const long long g = (long long)ii * n + jj;
+      sey = add(sey, mul(coef, x[g]));
+      sep = add(sep, mul(coef, x[Ntot + g]));
+    }
+  }
+  ay = add(sly, sey);
+  ap = add(slp, sep);
+}
+
+// residual rows (system.py:125-128)
+__device__ __forceinline__ void residual_rows(const Phys& P, double ay, double ap, double y, double p,
+                                              double f, double yd, double eps, double& r1, double& r2) {
+  const double ctrl = dvd(add(p, mul(P.mu, p_eps(dvd(-p, P.mu), eps))), P.nu);
+  r1 = add(sub(add(ay, phi_value(P, y)), f), ctrl);
+  r2 = add(sub(add(ap, mul(phi_d1(P, y), p)), y), yd);
+}
+
+// ---------------------------------------------------------------------------
+// gather v0 = x[pair_idx] into band order (schwarz.py:196)
+// ---------------------------------------------------------------------------
+__global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const double* x,
+                         double* pool) {
+  const SubInfo s = subs[list[blockIdx.x]];
+  double2* V = reinterpret_cast<double2*>(pool + s.loc);
+  const long long Ntot = (long long)P.n * P.n;
+  const int npts = s.NP / 2, real = s.nr * s.nc;
+  for (int q = threadIdx.x; q < npts; q += blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (q < real) {
+      int i, j;
+      local_to_global(s, q / s.nc, q % s.nc, i, j);
+      const long long g = (long long)i * P.n + j;
+      v = make_double2(x[g], x[Ntot + g]);
+    }
+    V[q] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// local residual (+ squared norm) of the listed subdomains at V + alpha_i D
+// _local_problem.local_residual (schwarz.py:181-186); R may be null (trial)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_residual(const SubInfo* subs, const int* list, Phys P,
+                                                  const double* x, const double* Vpool,
+                                                  const double* Dpool, const double* alpha,
+                                                  const double* f, const double* yd, double eps,
+                                                  double* Rpool, double* norm2) {
+  __shared__ double red[32];
+  const int sid = list[blockIdx.x];
+  const SubInfo s = subs[sid];
+  const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
+  const double2* D = Dpool ? reinterpret_cast<const double2*>(Dpool + s.loc) : nullptr;
+  double2* R = Rpool ? reinterpret_cast<double2*>(Rpool + s.loc) : nullptr;
+  const double a = alpha ? alpha[sid] : 0.0;
+  const long long Ntot = (long long)P.n * P.n;
+  const int real = s.nr * s.nc;
+  double acc = 0.0;
+  for (int q = threadIdx.x; q < real; q += blockDim.x) {
+    int i, j;
+    local_to_global(s, q / s.nc, q % s.nc, i, j);
+    double ay, ap;
+    stencil_point(s, P, V, D, a, x, Ntot, i, j, ay, ap);
+    const double2 v = lval(V, D, a, q);
+    const long long g = (long long)i * P.n + j;
+    double r1, r2;
+    residual_rows(P, ay, ap, v.x, v.y, f[g], yd[g], eps, r1, r2);
+    if (R) R[q] = make_double2(r1, r2);
+    acc = fma(r1, r1, acc);
+    acc = fma(r2, r2, acc);
+  }
+  const double tot = block_sum<256>(acc, red);
+  if (threadIdx.x == 0) norm2[sid] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobian diagonals per point (system.py:135-144) + the reference's finite
+// checks of phi'(y) and phi''(y) (system.py:56-74, check=True)
+// JD: 4 doubles per point: (4/h^2 + phi'(y), b12, b21, 0)
+// bad: per subdomain packed (which << 32 | first reference index), or -1
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_jacdiag(const SubInfo* subs, const int* list, Phys P,
+                                                 const double* Vpool, double eps, double* JDpool,
+                                                 long long* bad) {
+  const int sid = list[blockIdx.x];
+  const SubInfo s = subs[sid];
+  const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
+  double* JD = JDpool + 2 * s.loc;
+  const int real = s.nr * s.nc;
+  __shared__ unsigned long long first;
+  if (threadIdx.x == 0) first = ~0ull;
+  __syncthreads();
+  for (int q = threadIdx.x; q < real; q += blockDim.x) {
+    const double2 v = V[q];
+    const double y = v.x, p = v.y;
+    const double d1 = phi_d1(P, y);
+    const double d2 = phi_d2(P, y);
+    bool bad1 = !isfinite(d1), bad2 = !isfinite(d2);
+    if (P.phi_kind == 0 && P.kappa != 0.0 && mul(P.kappa, y) > 700.0) bad1 = bad2 = true;
+    if (P.phi_kind == 2 && y > 700.0) bad1 = bad2 = true;
+    if (bad1 || bad2) {
+      // reference index: row-major position in the rectangle
+      int i, j;
+      local_to_global(s, q / s.nc, q % s.nc, i, j);
+      const unsigned long long ref = (unsigned long long)((i - s.r0) * (s.c1 - s.c0) + (j - s.c0));
+      const unsigned long long key = ((bad1 ? 0ull : 1ull) << 32) | ref;
+      atomicMin(&first, key);
+    }
+    const double b12 = dvd(sub(1.0, dp_eps(dvd(-p, P.mu), eps)), P.nu);
+    const double b21 = sub(mul(d2, p), 1.0);
+    reinterpret_cast<double2*>(JD)[2 * q] = make_double2(add(P.diag, d1), b12);
+    reinterpret_cast<double2*>(JD)[2 * q + 1] = make_double2(b21, 0.0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) bad[sid] = first == ~0ull ? -1ll : (long long)first;
+}
+
+// ---------------------------------------------------------------------------
+// v += alpha_i d (newton.py:169) for the listed subdomains
+// ---------------------------------------------------------------------------
+__global__ void k_update(const SubInfo* subs, const int* list, double* Vpool, const double* Dpool,
+                         const double* alpha) {
+  const int sid = list[blockIdx.x];
+  const SubInfo s = subs[sid];
+  double2* V = reinterpret_cast<double2*>(Vpool + s.loc);
+  const double2* D = reinterpret_cast<const double2*>(Dpool + s.loc);
+  const double a = alpha[sid];
+  const int real = s.nr * s.nc;
+  for (int q = threadIdx.x; q < real; q += blockDim.x) {
+    double2 v = V[q];
+    const double2 d = D[q];
+    v.x = add(v.x, mul(a, d.x));
+    v.y = add(v.y, mul(a, d.y));
+    V[q] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// restricted prolongation: fval[own] = values[own_in_local] - x[own]
+// (_scatter_own + "- x", schwarz.py:247-250,317); grid (I, chunks)
+// ---------------------------------------------------------------------------
+__global__ void k_scatter_fval(const SubInfo* subs, Phys P, const double* Vpool, const double* x,
+                               double* fval) {
+  const SubInfo s = subs[blockIdx.x];
+  const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
+  const long long Ntot = (long long)P.n * P.n;
+  const int oc = s.oc1 - s.oc0, cnt = (s.or1 - s.or0) * oc;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < cnt; e += gridDim.y * blockDim.x) {
+    const int i = s.or0 + e / oc, j = s.oc0 + e % oc;
+    const long long g = (long long)i * P.n + j;
+    const double2 v = V[global_to_q(s, i, j)];
+    fval[g] = sub(v.x, x[g]);
+    fval[Ntot + g] = sub(v.y, x[Ntot + g]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// JVP right-hand side e = [a_ext @ dy; a_ext @ dp] in band order
+// (schwarz.py:341-342); zero away from the ring
+// ---------------------------------------------------------------------------
+__global__ void k_jvp_rhs(const SubInfo* subs, Phys P, const double* d, double* Bpool) {
+  const SubInfo s = subs[blockIdx.x];
+  double2* B = reinterpret_cast<double2*>(Bpool + s.loc);
+  const long long Ntot = (long long)P.n * P.n;
+  const int n = P.n, npts = s.NP / 2, real = s.nr * s.nc;
+  for (int q = threadIdx.x; q < npts; q += blockDim.x) {
+    double ey = 0.0, ep = 0.0;
+    if (q < real) {
+      int i, j;
+      local_to_global(s, q / s.nc, q % s.nc, i, j);
+      const int di[4] = {-1, 0, 0, 1};
+      const int dj[4] = {0, -1, 1, 0};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int ii = i + di[t], jj = j + dj[t];
+        if (ii < 0 || ii >= n || jj < 0 || jj >= n || in_rect(s, ii, jj)) continue;
+        const long long g = (long long)ii * n + jj;
+        ey = add(ey, mul(P.off, d[g]));
+        ep = add(ep, mul(P.off, d[Ntot + g]));
+      }
+    }
+    B[q] = make_double2(ey, ep);
+  }
+}
+
+// out[own] = -(d_loc + J^{-1} e)[own]   (schwarz.py:343-344)
+__global__ void k_jvp_out(const SubInfo* subs, Phys P, const double* d, const double* Zpool,
+                          double* out) {
+  const SubInfo s = subs[blockIdx.x];
+  const double2* Z = reinterpret_cast<const double2*>(Zpool + s.loc);
+  const long long Ntot = (long long)P.n * P.n;
+  const int oc = s.oc1 - s.oc0, cnt = (s.or1 - s.or0) * oc;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < cnt; e += gridDim.y * blockDim.x) {
+    const int i = s.or0 + e / oc, j = s.oc0 + e % oc;
+    const long long g = (long long)i * P.n + j;
+    const double2 z = Z[global_to_q(s, i, j)];
+    out[g] = -add(d[g], z.x);
+    out[Ntot + g] = -add(d[Ntot + g], z.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// layout conversion between the reference local layout ([y_loc; p_loc],
+// rectangle row-major) and band order
+// ---------------------------------------------------------------------------
+__global__ void k_ref_to_band(const SubInfo* subs, const double* ref, double* pool) {
+  const SubInfo s = subs[blockIdx.x];
+  const int C = s.c1 - s.c0, size = (s.r1 - s.r0) * C;
+  const double* src = ref + s.ref;
+  double2* V = reinterpret_cast<double2*>(pool + s.loc);
+  const int npts = s.NP / 2;
+  for (int q = threadIdx.x; q < npts; q += blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (q < size) {
+      int i, j;
+      local_to_global(s, q / s.nc, q % s.nc, i, j);
+      const int rr = (i - s.r0) * C + (j - s.c0);
+      v = make_double2(src[rr], src[size + rr]);
+    }
+    V[q] = v;
+  }
+}
+
+__global__ void k_band_to_ref(const SubInfo* subs, const double* pool, double* ref) {
+  const SubInfo s = subs[blockIdx.x];
+  const int C = s.c1 - s.c0, size = (s.r1 - s.r0) * C;
+  double* dst = ref + s.ref;
+  const double2* V = reinterpret_cast<const double2*>(pool + s.loc);
+  for (int rr = threadIdx.x; rr < size; rr += blockDim.x) {
+    const int i = s.r0 + rr / C, j = s.c0 + rr % C;
+    const double2 v = V[global_to_q(s, i, j)];
+    dst[rr] = v.x;
+    dst[size + rr] = v.y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vector kernels for GMRES (krylov.py), grid-stride, deterministic
+// "last block reduces" pattern: partials in fixed slots, the last block to
+// finish sums them in a fixed tree.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool last_block_done(unsigned int* counter) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int ticket = atomicAdd(counter, 1u);
+    is_last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  return is_last;
+}
+
+__device__ __forceinline__ void finish_reduction(double* partials, unsigned int* counter,
+                                                 double* result, bool take_sqrt, double* red) {
+  if (!last_block_done(counter)) return;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += partials[b];
+  const double tot = block_sum<RED_THREADS>(v, red);
+  if (threadIdx.x == 0) {
+    *result = take_sqrt ? sqrt(tot) : tot;
+    *counter = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_dot(long long n, const double* x, const double* y,
+                                                     double* partials, unsigned int* counter,
+                                                     double* result, int take_sqrt) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    acc = fma(x[e], y[e], acc);
+  const double tot = block_sum<RED_THREADS>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  finish_reduction(partials, counter, result, take_sqrt != 0, red);
+}
+
+// MGS pass i (krylov.py:113-116): w -= h_prev * q_prev (if has_prev), then
+// partial q_i . w (or ||w||^2 when q_i is null) -> h_out
+__global__ void __launch_bounds__(RED_THREADS) k_mgs_pass(long long n, double* w, const double* q_prev,
+                                                          const double* h_prev, const double* q_i,
+                                                          double* partials, unsigned int* counter,
+                                                          double* h_out) {
+  __shared__ double red[32];
+  const double hp = q_prev ? *h_prev : 0.0;
+  double acc = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    double we = w[e];
+    if (q_prev) {
+      we = sub(we, mul(hp, q_prev[e]));
+      w[e] = we;
+    }
+    acc = q_i ? fma(q_i[e], we, acc) : fma(we, we, acc);
+  }
+  const double tot = block_sum<RED_THREADS>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  finish_reduction(partials, counter, h_out, q_i == nullptr, red);
+}
+
+__global__ void k_add_scaled(long long n, const double* x, double alpha, const double* d, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = add(x[e], mul(alpha, d[e]));
+}
+
+__global__ void k_scale(long long n, double a, const double* x, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = mul(a, x[e]);
+}
+
+__global__ void k_div(long long n, const double* x, double s, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = dvd(x[e], s);
+}
+
+__global__ void k_flags(long long n, const double* x, const double* y, int* flag) {
+  // flag[0] cleared if x != y (bitwise, numpy.array_equal on floats: NaN != NaN);
+  // flag[1] cleared if x has a nonfinite entry
+  bool neq = false, nonfin = false;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double a = x[e];
+    if (y && !(a == y[e])) neq = true;
+    if (!isfinite(a)) nonfin = true;
+  }
+  if (__syncthreads_or(neq) && threadIdx.x == 0) flag[0] = 0;
+  if (__syncthreads_or(nonfin) && threadIdx.x == 0) flag[1] = 0;
+}
+
+// out = x + Q[:, :k] y, sum over columns in index order (krylov.py:151)
+__global__ void k_gemv_add(long long n, const double* Q, long long ldq, int k, const double* y,
+                           const double* x, double* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int c = 0; c < k; ++c) acc = fma(Q[c * ldq + e], y[c], acc);
+    out[e] = add(x[e], acc);
+  }
+}
+
+__global__ void k_recover_control(long long n, Phys P, const double* p, double eps, double* u) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double pe = p[e];
+    const double proj = eps == 0.0 ? fmin(fmax(dvd(-pe, P.mu), -1.0), 1.0)
+                                   : p_eps(dvd(-pe, P.mu), eps);
+    u[e] = dvd(-add(pe, mul(P.mu, proj)), P.nu);
+  }
+}
+
+}  // namespace ocp

@@ -1,0 +1,42 @@
+// Kernel declarations shared by the translation units.
+#pragma once
+#include "ocp_common.cuh"
+
+namespace ocp {
+
+__global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const double* x, double* pool);
+__global__ void k_residual(const SubInfo* subs, const int* list, Phys P, const double* x,
+                           const double* Vpool, const double* Dpool, const double* alpha,
+                           const double* f, const double* yd, double eps, double* Rpool,
+                           double* norm2);
+__global__ void k_jacdiag(const SubInfo* subs, const int* list, Phys P, const double* Vpool,
+                          double eps, double* JDpool, long long* bad);
+__global__ void k_update(const SubInfo* subs, const int* list, double* Vpool, const double* Dpool,
+                         const double* alpha);
+__global__ void k_scatter_fval(const SubInfo* subs, Phys P, const double* Vpool, const double* x,
+                               double* fval);
+__global__ void k_jvp_rhs(const SubInfo* subs, Phys P, const double* d, double* Bpool);
+__global__ void k_jvp_out(const SubInfo* subs, Phys P, const double* d, const double* Zpool,
+                          double* out);
+__global__ void k_ref_to_band(const SubInfo* subs, const double* ref, double* pool);
+__global__ void k_band_to_ref(const SubInfo* subs, const double* pool, double* ref);
+__global__ void k_dot(long long n, const double* x, const double* y, double* partials,
+                      unsigned int* counter, double* result, int take_sqrt);
+__global__ void k_mgs_pass(long long n, double* w, const double* q_prev, const double* h_prev,
+                           const double* q_i, double* partials, unsigned int* counter,
+                           double* h_out);
+__global__ void k_add_scaled(long long n, const double* x, double alpha, const double* d, double* out);
+__global__ void k_scale(long long n, double a, const double* x, double* out);
+__global__ void k_div(long long n, const double* x, double s, double* out);
+__global__ void k_flags(long long n, const double* x, const double* y, int* flag);
+__global__ void k_gemv_add(long long n, const double* Q, long long ldq, int k, const double* y,
+                           const double* x, double* out);
+__global__ void k_recover_control(long long n, Phys P, const double* p, double eps, double* u);
+
+__global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
+                              const double* JDpool, double* fac_pool, double* scratch,
+                              long long ws_stride, int* status);
+__global__ void k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool,
+                             const double* in_pool, double scale, double* out_pool);
+
+}  // namespace ocp
