@@ -376,10 +376,25 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(cudaMallocHost(&ctx->h_alpha, I * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_small, 8192 * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_flags, 4 * sizeof(int)));
-  CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           lu_smem_bytes(MAX_W)));
-  CKC(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024));
+  {
+    int optin = 0;
+    CKC(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa;
+    CKC(cudaFuncGetAttributes(&fa, k_band_factor));
+    if (lu_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
+      fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
+      return cleanup_fail(OCP_ERR_UNSUPPORTED);
+    }
+    CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             lu_smem_bytes(ctx->maxW)));
+    CKC(cudaFuncGetAttributes(&fa, k_band_solve));
+    const int solve_smem = ctx->maxNP * (int)sizeof(double);
+    if (solve_smem + (int)fa.sharedSizeBytes > optin) {
+      fail(ctx, OCP_ERR_UNSUPPORTED, "local system of %d unknowns exceeds shared memory", ctx->maxNP);
+      return cleanup_fail(OCP_ERR_UNSUPPORTED);
+    }
+    CKC(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem));
+  }
 #undef CKC
   for (auto& s : ctx->subs) ctx->dof_total += s.N;
   *out = ctx;
