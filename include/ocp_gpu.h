@@ -143,6 +143,10 @@ int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps,
 int ocp_set_profiling(ocp_ctx* ctx, int on);
 int ocp_stats(ocp_ctx* ctx, double* stats, int len);
 int ocp_reset_stats(ocp_ctx* ctx);
+/* CUDA events on the context stream (slot 0..15) for device-side timing of
+ * whole solves; elapsed milliseconds between two recorded slots. */
+int ocp_event_record(ocp_ctx* ctx, int slot);
+int ocp_event_elapsed(ocp_ctx* ctx, int slot_a, int slot_b, double* ms_host);
 
 #ifdef __cplusplus
 }

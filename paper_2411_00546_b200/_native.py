@@ -62,6 +62,8 @@ SIGNATURES = {
     "ocp_set_profiling": [_vp, _i],
     "ocp_stats": [_vp, _c_dbl_p, _i],
     "ocp_reset_stats": [_vp],
+    "ocp_event_record": [_vp, _i],
+    "ocp_event_elapsed": [_vp, _i, _i, _c_dbl_p],
 }
 _RESTYPES = {"ocp_ctx_destroy": None, "ocp_last_error": ctypes.c_char_p}
 

@@ -75,6 +75,7 @@ struct ocp_ctx {
   double stat_ms[6] = {0, 0, 0, 0, 0, 0};
   double stat_cnt[6] = {0, 0, 0, 0, 0, 0};
   double stat_flops = 0, stat_bytes = 0, stat_dof = 0;
+  cudaEvent_t marks[16] = {};
 };
 
 namespace {
@@ -419,6 +420,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
     cudaEventDestroy(e.b);
   }
   for (auto e : ctx->free_events) cudaEventDestroy(e);
+  for (auto e : ctx->marks) if (e) cudaEventDestroy(e);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -859,6 +861,23 @@ int ocp_reset_stats(ocp_ctx* ctx) {
   ctx->launches = 0;
   for (int i = 0; i < 6; ++i) ctx->stat_ms[i] = ctx->stat_cnt[i] = 0;
   ctx->stat_flops = ctx->stat_bytes = ctx->stat_dof = 0;
+  return OCP_OK;
+}
+
+int ocp_event_record(ocp_ctx* ctx, int slot) {
+  if (!ctx || slot < 0 || slot >= 16) return OCP_ERR_ARG;
+  if (!ctx->marks[slot]) CK(cudaEventCreate(&ctx->marks[slot]));
+  CK(cudaEventRecord(ctx->marks[slot], ctx->stream));
+  return OCP_OK;
+}
+
+int ocp_event_elapsed(ocp_ctx* ctx, int a, int b, double* ms) {
+  if (!ctx || a < 0 || a >= 16 || b < 0 || b >= 16 || !ctx->marks[a] || !ctx->marks[b])
+    return OCP_ERR_ARG;
+  CK(cudaEventSynchronize(ctx->marks[b]));
+  float f = 0.f;
+  CK(cudaEventElapsedTime(&f, ctx->marks[a], ctx->marks[b]));
+  *ms = f;
   return OCP_OK;
 }
 

@@ -87,6 +87,15 @@ class Engine:
                 "inner_solve_ms", "mgs_ms")
         return dict(zip(keys, list(buf)))
 
+    def mark(self, slot):
+        self.check(self.lib.ocp_event_record(self.ctx, slot), "ocp_event_record")
+
+    def elapsed_ms(self, a, b):
+        out = ctypes.c_double()
+        self.check(self.lib.ocp_event_elapsed(self.ctx, a, b, ctypes.byref(out)),
+                   "ocp_event_elapsed")
+        return out.value
+
     def reset_stats(self):
         self.check(self.lib.ocp_reset_stats(self.ctx), "ocp_reset_stats")
 

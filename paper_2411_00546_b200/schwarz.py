@@ -259,9 +259,20 @@ def raspen_solve(x0, dec, spec, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8
     report also carries ``per_subdomain_inner`` (per-evaluation lists of
     per-subdomain inner iterations; the reference keeps them internally).
     """
+    engine = build_local_systems(dec, spec)
+    x0 = np.asarray(x0, dtype=float)
+    x, report = solve_on_device(engine, engine.from_host(x0), sched, cfg, krylov_cfg, inner_tol,
+                                inner_max_outer, continuation, backtracking)
+    if x is None:
+        return np.array(x0, dtype=float, copy=True), report
+    return x.to_host(), report
+
+
+def solve_on_device(engine, x0, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8,
+                    inner_max_outer=200, continuation=True, backtracking=False):
+    """raspen_solve on a device-resident x0; returns (x DeviceVector or None on failure, report)."""
     cfg = cfg if cfg is not None else NewtonConfig()
     krylov_cfg = krylov_cfg if krylov_cfg is not None else KrylovConfig(rel_tol=1e-8, max_iters=400)
-    engine = build_local_systems(dec, spec)
     inner_cfg = NewtonConfig(tol=inner_tol, max_outer=inner_max_outer)
     eps_min = sched.eps_min
     fac = engine.factor_store()
@@ -299,16 +310,14 @@ def raspen_solve(x0, dec, spec, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8
     outer_cfg = NewtonConfig(tol=cfg.tol, max_outer=cfg.max_outer,
                              sigma=cfg.sigma if backtracking else math.inf,
                              max_halvings=cfg.max_halvings, linear_solver=krylov_cfg)
-    x0 = np.asarray(x0, dtype=float)
-    x0_dev = engine.from_host(x0)
     try:
-        x, report = newton_continuation(x0_dev, residual_fn, jacobian_fn,
+        x, report = newton_continuation(x0, residual_fn, jacobian_fn,
                                         ContinuationSchedule.fixed(eps_min), outer_cfg)
     except LocalSolveError as exc:
         report = SolveReport(False, max(state["evals"] - 1, 0),
                              inner_iters=list(state["inner_hist"]), failure=str(exc))
         report.per_subdomain_inner = list(state["per_sub"])
-        return np.array(x0, dtype=float, copy=True), report
+        return None, report
     report.inner_iters = list(state["inner_hist"])
     report.per_subdomain_inner = list(state["per_sub"])
-    return x.to_host(), report
+    return x, report
