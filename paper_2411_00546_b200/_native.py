@@ -116,21 +116,77 @@ def ptr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+class BufferPool:
+    """Per-engine caching allocator (one CUDA stream per engine => reuse is stream-ordered).
+
+    cudaFree synchronises the device; GMRES allocates a fresh vector per
+    matvec, so freed buffers are cached by size and handed out again.
+    """
+
+    def __init__(self, limit_bytes=48 << 30):
+        self.free = {}
+        self.cached = 0
+        self.limit = limit_bytes
+        self.closed = False
+
+    def take(self, nbytes):
+        lst = self.free.get(nbytes)
+        if lst:
+            self.cached -= nbytes
+            return lst.pop()
+        return None
+
+    def give(self, addr, nbytes):
+        if self.closed or self.cached + nbytes > self.limit:
+            _raw_free(addr)
+            return
+        self.free.setdefault(nbytes, []).append(addr)
+        self.cached += nbytes
+
+    def release_all(self):
+        self.closed = True
+        for lst in self.free.values():
+            for addr in lst:
+                _raw_free(addr)
+        self.free.clear()
+        self.cached = 0
+
+
+def _raw_alloc(nbytes):
+    lib = load()
+    p = ctypes.c_void_p()
+    rc = lib.ocp_malloc(ctypes.c_size_t(nbytes), ctypes.byref(p))
+    if rc != OCP_OK:
+        raise NativeError(rc, last_error(), "ocp_malloc")
+    return p.value
+
+
+def _raw_free(addr):
+    if _lib is not None and addr:
+        _lib.ocp_free(ctypes.c_void_p(addr))
+
+
 class DeviceBuffer:
-    """Raw device allocation owned by Python (freed on collection)."""
+    """Device allocation owned by Python; returns to its pool (or is freed) on collection."""
 
-    __slots__ = ("addr", "nbytes", "__weakref__")
+    __slots__ = ("addr", "nbytes", "pool", "__weakref__")
 
-    def __init__(self, nbytes):
-        lib = load()
-        p = ctypes.c_void_p()
-        rc = lib.ocp_malloc(ctypes.c_size_t(max(int(nbytes), 16)), ctypes.byref(p))
-        if rc != OCP_OK:
-            raise NativeError(rc, last_error(), "ocp_malloc")
-        self.addr = p.value
-        self.nbytes = int(nbytes)
+    def __init__(self, nbytes, pool=None):
+        nbytes = max(int(nbytes), 16)
+        nbytes = (nbytes + 255) // 256 * 256
+        self.pool = pool
+        addr = pool.take(nbytes) if pool is not None else None
+        if addr is None:
+            addr = _raw_alloc(nbytes)
+        self.addr = addr
+        self.nbytes = nbytes
 
     def __del__(self):
-        if getattr(self, "addr", None) and _lib is not None:
-            _lib.ocp_free(ctypes.c_void_p(self.addr))
-            self.addr = None
+        addr = getattr(self, "addr", None)
+        if not addr:
+            return
+        self.addr = None
+        if self.pool is not None:
+            self.pool.give(addr, self.nbytes)
+        else:
+            _raw_free(addr)

@@ -173,7 +173,7 @@ double band_lu_flops(long long N, long long w) {
   return tot;
 }
 
-int lu_smem_bytes(int W) { return (NB * (NB + W + 1) + NB * W) * (int)sizeof(double); }
+int lu_smem_bytes(int W) { return (NB * (NB + W + 1) + NB * W + 2 * NB * NB) * (int)sizeof(double); }
 
 int upload_list(ocp_ctx* ctx, const std::vector<int>& list) {
   std::copy(list.begin(), list.end(), ctx->h_list);
@@ -202,9 +202,8 @@ int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, 
   double bytes = 0;
   for (int i : list) bytes += ctx->sub_fbytes[i];
   Timer t(ctx, cls, 0, bytes);
-  k_band_solve<<<cnt, 256, ctx->maxNP * sizeof(double), ctx->stream>>>(ctx->d_subs, d_list, fac, in,
-                                                                       scale, out);
-  CKL();
+  CK(launch_band_solve(0, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out, ctx->maxW));
+  ++ctx->launches;
   return OCP_OK;
 }
 
@@ -289,7 +288,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       s.fac = fac;
       s.ref = ref;
       loc += s.NP;
-      fac += (long long)s.NP * (2 * s.W + 1);
+      fac += (long long)s.NP * 2 * (s.W + 1);
       ref += s.N;
       ctx->subs.push_back(s);
       ctx->sub_flops.push_back(band_lu_flops(s.N, s.w));
@@ -307,12 +306,6 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   if (ctx->maxW > MAX_W) {
     int code = fail(nullptr, OCP_ERR_UNSUPPORTED,
                     "local half-bandwidth %d exceeds the compiled limit %d", ctx->maxW, MAX_W);
-    delete ctx;
-    return code;
-  }
-  if ((long long)ctx->maxNP * 8 > 227 * 1024) {
-    int code = fail(nullptr, OCP_ERR_UNSUPPORTED, "local system of %d unknowns exceeds shared memory",
-                    ctx->maxNP);
     delete ctx;
     return code;
   }
@@ -388,13 +381,12 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     }
     CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              lu_smem_bytes(ctx->maxW)));
-    CKC(cudaFuncGetAttributes(&fa, k_band_solve));
-    const int solve_smem = ctx->maxNP * (int)sizeof(double);
-    if (solve_smem + (int)fa.sharedSizeBytes > optin) {
-      fail(ctx, OCP_ERR_UNSUPPORTED, "local system of %d unknowns exceeds shared memory", ctx->maxNP);
+    const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
+    if (solve_smem > optin) {
+      fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");
       return cleanup_fail(OCP_ERR_UNSUPPORTED);
     }
-    CKC(cudaFuncSetAttribute(k_band_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_smem));
+    CKC(set_band_solve_smem(solve_smem));
   }
 #undef CKC
   for (auto& s : ctx->subs) ctx->dof_total += s.N;
@@ -663,13 +655,18 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
   if (!ctx || !fac || !d || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
-  Timer t(ctx, CLS_JVP);
-  k_jvp_rhs<<<I, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B);
+  Timer tj(ctx, CLS_JVP);
+  const dim3 grid(I, 4);
+  k_jvp_rhs<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B);
   CKL();
-  std::vector<int> all(I);
-  for (int i = 0; i < I; ++i) all[i] = i;
-  if (int rc = launch_solve(ctx, ctx->d_list_all, all, fac, ctx->B, 1.0, ctx->B, CLS_SOLVE)) return rc;
-  dim3 grid(I, 8);
+  {
+    double bytes = 0;
+    for (int i = 0; i < I; ++i) bytes += ctx->sub_fbytes[i];
+    Timer t(ctx, CLS_SOLVE, 0, bytes);
+    CK(launch_band_solve(1, I, st, ctx->d_subs, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B,
+                         ctx->maxW));
+    ++ctx->launches;
+  }
   k_jvp_out<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B, out);
   CKL();
   return OCP_OK;

@@ -16,7 +16,11 @@
 // trailing update is a rank-NB register-tiled FP64 FMA update (4x4 per
 // thread).  Finished L columns / U rows stream to the factor store in the
 // panel-block layout the solve kernel reads linearly:
-//   block K: [L: NB x W  (L[k0+c+1+s][k0+c])][U: NB x (W+1)  (U[k0+c][k0+c+s])]
+//   block K: [L: NB x (W+1) (L[k0+c+1+s][k0+c], s < W; slot W unused)]
+//            [U: NB x (W+1) (U[k0+c][k0+c+s])]
+// with the in-block triangles replaced by their inverses: L entries with
+// c+1+s < NB hold (L11^{-1})[c+1+s][c], U entries with c+s < NB hold
+// (U11^{-1})[c][c+s].
 #include "ocp_kernels.cuh"
 
 namespace ocp {
@@ -55,6 +59,8 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doubl
     double* fac = fac_pool + s.fac;
     double* Pt = sm;                  // Pt[t*LDP + r]: panel column t, row k0 + r
     double* Us = sm + NB * LDP;       // Us[t*W + c]: row k0 + t, column k0 + NB + c
+    double* Li = Us + NB * W;         // Li[i*NB + j] = (L11^{-1})[i][j]
+    double* Ui = Li + NB * NB;        // Ui[i*NB + j] = (U11^{-1})[i][j]
     if (tid == 0) bad = 0;
     for (int e = tid; e < WS * WS; e += blockDim.x) {
       const int i = e / WS, j = e - (e / WS) * WS;
@@ -87,20 +93,51 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doubl
         }
         __syncthreads();
       }
-      // 3. U12 = L11^{-1} A12, one thread per column
-      for (int c = tid; c < W; c += blockDim.x) {
-        double u[NB];
+      // 3. U12 = L11^{-1} A12, one thread per column; 32 more threads form the
+      //    16x16 triangular inverses of L11 and U11, which the solve kernel
+      //    applies as small mat-vecs instead of serial substitutions
+      for (int c = tid; c < W + 2 * NB; c += blockDim.x) {
+        if (c < W) {
+          double u[NB];
 #pragma unroll
-        for (int t = 0; t < NB; ++t) u[t] = Us[t * W + c];
+          for (int t = 0; t < NB; ++t) u[t] = Us[t * W + c];
 #pragma unroll
-        for (int t = 1; t < NB; ++t) {
-          double acc = u[t];
+          for (int t = 1; t < NB; ++t) {
+            double acc = u[t];
 #pragma unroll
-          for (int q = 0; q < t; ++q) acc = fma(-Pt[q * LDP + t], u[q], acc);
-          u[t] = acc;
+            for (int q = 0; q < t; ++q) acc = fma(-Pt[q * LDP + t], u[q], acc);
+            u[t] = acc;
+          }
+#pragma unroll
+          for (int t = 0; t < NB; ++t) Us[t * W + c] = u[t];
+        } else if (c < W + NB) {
+          const int j = c - W;  // column j of L11^{-1} (unit lower)
+          double x[NB];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            double acc = (i == j) ? 1.0 : 0.0;
+            if (i > j) {
+#pragma unroll
+              for (int k = 0; k < i; ++k)
+                if (k >= j) acc = fma(-Pt[k * LDP + i], x[k], acc);
+            }
+            x[i] = acc;
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) Li[i * NB + j] = x[i];
+        } else {
+          const int j = c - W - NB;  // column j of U11^{-1} (upper)
+          double x[NB];
+#pragma unroll
+          for (int i = NB - 1; i >= 0; --i) {
+            double acc = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+            for (int k = i + 1; k < NB; ++k) acc = fma(-Pt[k * LDP + i], x[k], acc);
+            x[i] = (i <= j) ? acc / Pt[i * LDP + i] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < NB; ++i) Ui[i * NB + j] = x[i];
         }
-#pragma unroll
-        for (int t = 0; t < NB; ++t) Us[t * W + c] = u[t];
       }
       __syncthreads();
       // 4. trailing update A22 -= L21 U12 on [k0+NB, k0+NB+W)^2, 4x4 tiles
@@ -137,15 +174,17 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doubl
         }
       }
       // 5. stream the finished panel block to the factor store
-      double* Lb = fac + (long long)K * NB * (2 * W + 1);
-      double* Ub = Lb + NB * W;
-      for (int e = tid; e < NB * W; e += blockDim.x) {
-        const int c = e / W, sidx = e % W;
-        Lb[e] = Pt[c * LDP + c + 1 + sidx];
+      double* Lb = fac + (long long)K * NB * 2 * (W + 1);
+      double* Ub = Lb + NB * (W + 1);
+      for (int e = tid; e < NB * (W + 1); e += blockDim.x) {
+        const int c = e / (W + 1), sidx = e % (W + 1);
+        Lb[e] = sidx == W ? 0.0
+                          : (sidx < NB - 1 - c) ? Li[(c + 1 + sidx) * NB + c]
+                                                : Pt[c * LDP + c + 1 + sidx];
       }
       for (int e = tid; e < NB * (W + 1); e += blockDim.x) {
         const int c = e / (W + 1), sidx = e % (W + 1);
-        Ub[e] = (c + sidx < NB) ? Pt[(c + sidx) * LDP + c] : Us[c * W + c + sidx - NB];
+        Ub[e] = (c + sidx < NB) ? Ui[c * NB + c + sidx] : Us[c * W + c + sidx - NB];
       }
       // 6. original entries entering the window for panel K+1 (they reuse the
       //    physical slots of panel K, already copied to shared memory)
@@ -170,86 +209,6 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doubl
     if (tid == 0) status[sid] = bad;
     __syncthreads();
   }
-}
-
-// ---------------------------------------------------------------------------
-// Forward + backward substitution with the stored factors, one CTA per
-// listed subdomain, the whole vector in shared memory.
-// out = L U \ (scale * in)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
-             double scale, double* out_pool) {
-  extern __shared__ double xs[];
-  __shared__ double part[NB];
-  const SubInfo s = subs[list[blockIdx.x]];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int W = s.W, NP = s.NP, nblk = NP / NB;
-  const long long bstride = (long long)NB * (2 * W + 1);
-  const double* fac = fac_pool + s.fac;
-  const double* in = in_pool + s.loc;
-  double* out = out_pool + s.loc;
-  for (int e = tid; e < NP; e += blockDim.x) xs[e] = scale * in[e];
-  __syncthreads();
-  // forward: unit lower L, column blocks
-  for (int K = 0; K < nblk; ++K) {
-    const int k0 = K * NB;
-    const double* L = fac + K * bstride;
-    if (warp == 0) {
-      double xr = lane < NB ? xs[k0 + lane] : 0.0;
-#pragma unroll
-      for (int c = 0; c < NB - 1; ++c) {
-        const double xc = __shfl_sync(0xffffffffu, xr, c);
-        if (lane > c && lane < NB) xr = fma(-L[c * W + (lane - c - 1)], xc, xr);
-      }
-      if (lane < NB) xs[k0 + lane] = xr;
-    }
-    __syncthreads();
-    for (int sp = tid; sp < W; sp += blockDim.x) {
-      const int row = k0 + NB + sp;
-      if (row < NP) {
-        double acc = xs[row];
-#pragma unroll
-        for (int c = 0; c < NB; ++c) {
-          const int idx = NB + sp - c - 1;
-          if (idx < W) acc = fma(-L[c * W + idx], xs[k0 + c], acc);
-        }
-        xs[row] = acc;
-      }
-    }
-    __syncthreads();
-  }
-  // backward: U row blocks, last to first
-  for (int K = nblk - 1; K >= 0; --K) {
-    const int k0 = K * NB;
-    const double* U = fac + K * bstride + NB * W;
-    {
-      const int c = tid >> 4, t = tid & 15;
-      double acc = 0.0;
-      if (c < NB) {
-        for (int sidx = NB - c + t; sidx <= W; sidx += 16) {
-          const int col = k0 + c + sidx;
-          if (col < NP) acc = fma(U[c * (W + 1) + sidx], xs[col], acc);
-        }
-      }
-#pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (t == 0 && c < NB) part[c] = acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double a = lane < NB ? xs[k0 + lane] - part[lane] : 0.0;
-#pragma unroll
-      for (int c = NB - 1; c >= 0; --c) {
-        if (lane == c) a = a / U[c * (W + 1)];
-        const double xc = __shfl_sync(0xffffffffu, a, c);
-        if (lane < c) a = fma(-U[lane * (W + 1) + (c - lane)], xc, a);
-      }
-      if (lane < NB) xs[k0 + lane] = a;
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < NP; e += blockDim.x) out[e] = xs[e];
 }
 
 }  // namespace ocp

@@ -227,7 +227,7 @@ __global__ void k_jvp_rhs(const SubInfo* subs, Phys P, const double* d, double* 
   double2* B = reinterpret_cast<double2*>(Bpool + s.loc);
   const long long Ntot = (long long)P.n * P.n;
   const int n = P.n, npts = s.NP / 2, real = s.nr * s.nc;
-  for (int q = threadIdx.x; q < npts; q += blockDim.x) {
+  for (int q = blockIdx.y * blockDim.x + threadIdx.x; q < npts; q += gridDim.y * blockDim.x) {
     double ey = 0.0, ep = 0.0;
     if (q < real) {
       int i, j;

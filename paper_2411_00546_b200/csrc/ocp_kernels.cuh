@@ -36,7 +36,11 @@ __global__ void k_recover_control(long long n, Phys P, const double* p, double e
 __global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
                               const double* JDpool, double* fac_pool, double* scratch,
                               long long ws_stride, int* status);
-__global__ void k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool,
-                             const double* in_pool, double scale, double* out_pool);
+// banded solve (ocp_solve.cu): mode 0 pool -> pool, mode 1 fused JVP
+size_t solve_smem_bytes(int max_w);
+cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
+                              const int* list, const double* fac, const double* in, double scale,
+                              double* out_pool, int max_w);
+cudaError_t set_band_solve_smem(int bytes);
 
 }  // namespace ocp

@@ -1,0 +1,250 @@
+// Banded forward/backward solve with the stored local factors (sm_100a, FP64).
+//
+// Replaces SuperLU.solve (newton.py:127 for the inner Newton direction,
+// schwarz.py:343 inside raspen_jacobian_apply).  One CTA per subdomain:
+//
+//   * the factor blocks ([L | U] per panel of NB unknowns, ocp_band.cu) stream
+//     from HBM through a STAGES-deep ring of shared-memory buffers filled by
+//     TMA bulk copies (cp.async.bulk + mbarrier complete_tx), issued STAGES
+//     blocks ahead of use;
+//   * the active part of the vector (W + 2 NB entries) lives in a circular
+//     shared buffer; finished forward values go to the output vector and
+//     come back for the backward sweep;
+//   * the in-block triangles were inverted at factorisation time, so each
+//     block costs two barrier-separated phases of independent FMAs:
+//       forward  y_K = L11^{-1} b_K ;  b_{K+1..} -= L21 y_K
+//       backward x_K = U11^{-1} (z_K - U12 x_{K+1..})
+//
+// rhs = scale * in_pool, solution -> out_pool (band order; in place allowed).
+// Every global access on the per-block critical path is prefetched one
+// block ahead (entering rhs rows, z of the next backward block).
+// MODE 1 (JVP): only the ownership block of the solution is consumed
+// (schwarz.py:344), so the backward sweep stops above the first owned row.
+#include <cstdint>
+
+#include "ocp_kernels.cuh"
+
+namespace ocp {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LAB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra LAB_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// circular vector window: >= W + 2 NB entries, power of two (index by mask)
+__host__ __device__ __forceinline__ int ring_size(int w) {
+  int r = 64;
+  while (r < w + 2 * NB) r <<= 1;
+  return r;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2)
+k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
+             double scale, double* out_pool, int max_w) {
+  extern __shared__ __align__(16) double smem[];
+  const int SB = NB * (max_w + 1);                  // doubles per stage
+  const int RMAX = ring_size(max_w);
+  double* stage = smem;                             // SOLVE_STAGES x SB
+  double* ring = smem + SOLVE_STAGES * SB;          // RMAX (power of two)
+  double* ys = ring + RMAX;                         // NB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ys + NB);  // 2 x SOLVE_STAGES
+
+  const SubInfo s = subs[list[blockIdx.x]];
+  const int tid = threadIdx.x;
+  const int W = s.W, LD = W + 1, NP = s.NP, nblk = NP / NB;
+  const int RM = ring_size(W) - 1;                  // ring index mask
+  const long long bstride = 2LL * NB * LD;
+  const double* fac = fac_pool + s.fac;
+  double* zx = out_pool + s.loc;                    // z after the forward sweep, x after the backward
+  const double* in = in_pool + s.loc;
+  const int gi = tid >> 4, gj = tid & 15;           // 16 x 16 thread grid for the block mat-vecs
+
+  if (tid == 0) {
+    for (int st = 0; st < 2 * SOLVE_STAGES; ++st) mbar_init(&bars[st], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int k = tid; k <= RM; k += blockDim.x) ring[k] = 0.0;
+  __syncthreads();
+  // ---------------- forward: L y = b ----------------
+  const uint32_t lbytes = (uint32_t)(NB * LD * sizeof(double));
+  if (tid == 0) {
+    for (int st = 0; st < SOLVE_STAGES && st < nblk; ++st) {
+      mbar_expect_tx(&bars[st], lbytes);
+      bulk_g2s(stage + st * SB, fac + st * bstride, lbytes, &bars[st]);
+    }
+  }
+  for (int k = tid; k < W + NB && k < NP; k += blockDim.x) ring[k & RM] = scale * in[k];
+  // rows entering the window at step K are [k0+NB+W, k0+2NB+W): prefetched one step ahead
+  double rreg = 0.0;
+  if (tid < NB && NB + W + tid < NP) rreg = in[NB + W + tid];
+  __syncthreads();
+  for (int K = 0; K < nblk; ++K) {
+    const int k0 = K * NB, st = K % SOLVE_STAGES;
+    const double* Lb = stage + st * SB;
+    mbar_wait(&bars[st], (K / SOLVE_STAGES) & 1);
+    {  // y_K = L11^{-1} b_K   (row gi, 16 lanes reduce over gj)
+      const double bj = ring[(k0 + gj) & RM];
+      const double l = Lb[gj * LD + ((gi - gj - 1) & 15)];
+      double v = gj < gi ? l * bj : (gj == gi ? bj : 0.0);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (gj == 0) ys[gi] = v;
+    }
+    __syncthreads();
+    if (tid < NB) {
+      const double y = ys[tid];
+      ring[(k0 + tid) & RM] = y;
+      zx[k0 + tid] = y;
+      const int r = k0 + NB + W + tid;               // entering row (slot of k0 - NB + tid)
+      if (r < NP) ring[r & RM] = scale * rreg;
+      const int rn = r + NB;
+      rreg = rn < NP ? in[rn] : 0.0;
+    }
+    {  // b_r -= L21 y_K, r = k0 + NB + t
+      const int t = tid;
+      const int r = k0 + NB + t;
+      if (t < W && r < NP) {
+        const double* lp = Lb + (NB - 1) + t;        // column c entry at lp + c * (LD - 1)
+        double acc = ring[r & RM];
+        if (t + NB <= W) {
+#pragma unroll
+          for (int c = 0; c < NB; ++c) acc = fma(-lp[c * (LD - 1)], ys[c], acc);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (NB - 1 + t - c < W) acc = fma(-lp[c * (LD - 1)], ys[c], acc);
+        }
+        ring[r & RM] = acc;
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && K + SOLVE_STAGES < nblk) {
+      mbar_expect_tx(&bars[st], lbytes);
+      bulk_g2s(stage + st * SB, fac + (K + SOLVE_STAGES) * bstride, lbytes, &bars[st]);
+    }
+  }
+  // ---------------- backward: U x = z ----------------
+  int kstop = 0;  // first row whose solution is needed
+  if (MODE == 1) {
+    const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+    kstop = 2 * s.nc * a_own;
+  }
+  const uint32_t ubytes = (uint32_t)(NB * LD * sizeof(double));
+  uint64_t* ubars = bars + SOLVE_STAGES;
+  if (tid == 0) {
+    for (int st = 0; st < SOLVE_STAGES && st < nblk; ++st) {
+      const int K = nblk - 1 - st;
+      mbar_expect_tx(&ubars[st], ubytes);
+      bulk_g2s(stage + st * SB, fac + K * bstride + NB * LD, ubytes, &ubars[st]);
+    }
+  }
+  // ring slots of indices >= NP must read as 0 (their U entries are 0 too)
+  for (int k = NP + tid; k < NP + W + NB; k += blockDim.x) ring[k & RM] = 0.0;
+  __syncthreads();
+  // z of block K is in the ring when step K starts; z of K-1 is held in a
+  // register one step ahead
+  if (tid < NB) ring[(NP - NB + tid) & RM] = zx[NP - NB + tid];
+  double zreg = (tid < NB && nblk >= 2) ? zx[NP - 2 * NB + tid] : 0.0;
+  const int MW = W / 16 + 1;  // band columns per lane (stride 16)
+  __syncthreads();
+  int step = 0;
+  for (; step < nblk; ++step) {
+    const int K = nblk - 1 - step, k0 = K * NB, st = step % SOLVE_STAGES;
+    if (k0 + NB <= kstop) break;
+    const double* Ub = stage + st * SB;
+    mbar_wait(&ubars[st], (step / SOLVE_STAGES) & 1);
+    {  // r_c = z_c - U12 x   (row gi, lanes gj stride 16 over the band)
+      double acc = 0.0;
+      const double* up = Ub + gi * LD;
+      const int base = k0 + gi;
+#pragma unroll 4
+      for (int m = 0; m < MW; ++m) {
+        const int sidx = NB - gi + gj + 16 * m;
+        if (sidx <= W) acc = fma(up[sidx], ring[(base + sidx) & RM], acc);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (gj == 0) ys[gi] = ring[(k0 + gi) & RM] - acc;
+    }
+    __syncthreads();
+    {  // x_K = U11^{-1} r
+      const double u = Ub[gi * LD + ((gj - gi) & 15)];
+      double v = gj >= gi ? u * ys[gj] : 0.0;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (gj == 0) {
+        ring[(k0 + gi) & RM] = v;
+        zx[k0 + gi] = v;
+      }
+    }
+    if (tid < NB && k0 >= NB) {
+      ring[(k0 - NB + tid) & RM] = zreg;
+      zreg = k0 >= 2 * NB ? zx[k0 - 2 * NB + tid] : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0 && step + SOLVE_STAGES < nblk) {
+      const int Kn = nblk - 1 - (step + SOLVE_STAGES);
+      mbar_expect_tx(&ubars[st], ubytes);
+      bulk_g2s(stage + st * SB, fac + Kn * bstride + NB * LD, ubytes, &ubars[st]);
+    }
+  }
+  // an early stop leaves up to SOLVE_STAGES bulk copies in flight: wait for
+  // them before the CTA (and its shared memory) retires
+  for (int s2 = step; s2 < nblk && s2 < step + SOLVE_STAGES; ++s2)
+    mbar_wait(&ubars[s2 % SOLVE_STAGES], (s2 / SOLVE_STAGES) & 1);
+}
+
+size_t solve_smem_bytes(int max_w) {
+  return sizeof(double) * ((size_t)SOLVE_STAGES * NB * (max_w + 1) + ring_size(max_w) + NB) +
+         sizeof(uint64_t) * 2 * SOLVE_STAGES;
+}
+
+cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
+                              const int* list, const double* fac, const double* in, double scale,
+                              double* out_pool, int max_w) {
+  const size_t smem = solve_smem_bytes(max_w);
+  if (mode == 0)
+    k_band_solve<0><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, max_w);
+  else
+    k_band_solve<1><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, max_w);
+  return cudaGetLastError();
+}
+
+cudaError_t set_band_solve_smem(int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(k_band_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_band_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace ocp

@@ -14,6 +14,12 @@ from . import _native as nat
 from .system import phi_code
 
 
+def _destroy(lib, ctx, pool):
+    lib.ocp_sync(ctx)
+    pool.release_all()
+    lib.ocp_ctx_destroy(ctx)
+
+
 class Engine:
     """Native context for one problem + s1 x s2 decomposition with overlap m."""
 
@@ -38,7 +44,8 @@ class Engine:
                 raise nat.NativeUnavailable(msg)
             raise nat.NativeError(rc, msg, "ocp_ctx_create")
         self.ctx = ctx
-        self._finalizer = weakref.finalize(self, lib.ocp_ctx_destroy, ctx)
+        self.pool = nat.BufferPool()
+        self._finalizer = weakref.finalize(self, _destroy, lib, ctx, self.pool)
         info = (ctypes.c_longlong * 8)()
         nat.check(lib.ocp_ctx_info(ctx, info), ctx, "ocp_ctx_info")
         self.num_subdomains = int(info[0])
@@ -73,7 +80,10 @@ class Engine:
         return v
 
     def factor_store(self):
-        return nat.DeviceBuffer(8 * self.fac_len)
+        return nat.DeviceBuffer(8 * self.fac_len, self.pool)
+
+    def buffer(self, nbytes):
+        return nat.DeviceBuffer(nbytes, self.pool)
 
     # -- instrumentation ---------------------------------------------------
     def set_profiling(self, on):
@@ -108,7 +118,7 @@ class DeviceVector:
     def __init__(self, engine, n, buf=None):
         self.engine = engine
         self.n = int(n)
-        self.buf = buf if buf is not None else nat.DeviceBuffer(8 * self.n)
+        self.buf = buf if buf is not None else nat.DeviceBuffer(8 * self.n, engine.pool)
 
     @property
     def ptr(self):
@@ -231,7 +241,7 @@ class DeviceBasis:
         self.engine = engine
         self.n = n
         self.cap = cap
-        self.buf = nat.DeviceBuffer(8 * n * (cap + 1))
+        self.buf = nat.DeviceBuffer(8 * n * (cap + 1), engine.pool)
 
     def column(self, j):
         v = DeviceVector.__new__(DeviceVector)
@@ -242,7 +252,7 @@ class DeviceBasis:
 
     def grow(self, cap, used):
         e = self.engine
-        new = nat.DeviceBuffer(8 * self.n * (cap + 1))
+        new = nat.DeviceBuffer(8 * self.n * (cap + 1), e.pool)
         e.check(e.lib.ocp_d2d(e.ctx, ctypes.c_void_p(new.addr), ctypes.c_void_p(self.buf.addr),
                               8 * self.n * used), "ocp_d2d")
         e.sync()

@@ -37,3 +37,15 @@ for r in range(reps):
               f"jvp-solve {st['solve_bytes']/max(st['solve_ms'],1e-9)/1e6:.1f} GB/s over {st['solve_launches']:.0f}")
 if x is not None and len(sys.argv) > 4:
     np.save(sys.argv[4], x.to_host())
+
+if len(sys.argv) > 5 and sys.argv[5] == "profile":
+    import cProfile
+    import pstats
+    pr = cProfile.Profile()
+    pr.enable()
+    t0 = time.perf_counter()
+    x, rep = solve_on_device(eng, x0, sched, NewtonConfig(tol=1e-10), KrylovConfig(rel_tol=1e-8, max_iters=1000), inner_tol, 200)
+    eng.sync()
+    pr.disable()
+    print(f"profiled wall {time.perf_counter()-t0:.3f}s")
+    pstats.Stats(pr).sort_stats("tottime").print_stats(15)
