@@ -127,6 +127,12 @@ int ocp_vec_all_finite(ocp_ctx* ctx, long long n, const double* x, int* finite_h
  * h_host receives j+2 values. */
 int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j,
             double* w, double* h_host);
+/* One whole Arnoldi step (krylov.py:110-122): MGS of w_in = A q_j against
+ * Q[:, 0..j] (w_in is not modified), h_host[0..j+1], and
+ * Q[:, j+1] = w / h[j+1] (written even on a happy breakdown; unused then).
+ * Single cooperative kernel; falls back to per-pass kernels for large n. */
+int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j,
+                const double* w_in, double* h_host);
 /* out = x + Q[:, :k] @ y  (krylov.py:151) */
 int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k,
                  const double* y_host, const double* x, double* out);

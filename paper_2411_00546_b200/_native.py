@@ -57,6 +57,7 @@ SIGNATURES = {
     "ocp_vec_equal": [_vp, _ll, _vp, _vp, _c_int_p],
     "ocp_vec_all_finite": [_vp, _ll, _vp, _c_int_p],
     "ocp_mgs": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
+    "ocp_arnoldi": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
     "ocp_gemv_add": [_vp, _ll, _vp, _ll, _i, _c_dbl_p, _vp, _vp],
     "ocp_recover_control": [_vp, _ll, _vp, _d, _vp],
     "ocp_set_profiling": [_vp, _i],

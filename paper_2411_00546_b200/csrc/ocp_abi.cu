@@ -814,6 +814,47 @@ int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j, do
   return OCP_OK;
 }
 
+int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j, const double* w_in,
+                double* h_host) {
+  if (j + 2 > ctx->h_cap) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->d_h));
+    ctx->h_cap = 2 * (j + 2);
+    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+  }
+  cudaStream_t st = ctx->stream;
+  {
+    Timer t(ctx, CLS_MGS);
+    cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, ldq, j, w_in, ctx->red_partials, ctx->d_h);
+    if (e == cudaSuccess) {
+      ++ctx->launches;
+    } else if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      double* w = Q + (long long)(j + 1) * ldq;  // work in the next column
+      CK(cudaMemcpyAsync(w, w_in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      for (int i = 0; i <= j; ++i) {
+        k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(
+            n, w, i > 0 ? Q + (long long)(i - 1) * ldq : nullptr, i > 0 ? ctx->d_h + i - 1 : nullptr,
+            Q + (long long)i * ldq, ctx->red_partials, ctx->red_counter, ctx->d_h + i);
+        CKL();
+      }
+      k_mgs_pass<<<RED_BLOCKS, RED_THREADS, 0, st>>>(n, w, Q + (long long)j * ldq, ctx->d_h + j,
+                                                     nullptr, ctx->red_partials, ctx->red_counter,
+                                                     ctx->d_h + j + 1);
+      CKL();
+      CK(cudaMemcpyAsync(ctx->h_small, ctx->d_h + j + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      k_div<<<ew_grid(n), 256, 0, st>>>(n, w, ctx->h_small[0], w);
+      CKL();
+    } else {
+      return fail(ctx, OCP_ERR_CUDA, "cooperative Arnoldi launch: %s", cudaGetErrorString(e));
+    }
+  }
+  CK(cudaMemcpyAsync(h_host, ctx->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return OCP_OK;
+}
+
 int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k, const double* y_host,
                  const double* x, double* out) {
   if (k + 2 > ctx->h_cap) {

@@ -42,5 +42,9 @@ cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo
                               const int* list, const double* fac, const double* in, double scale,
                               double* out_pool, int max_w);
 cudaError_t set_band_solve_smem(int bytes);
+// one full MGS Arnoldi step (ocp_krylov.cu); cudaErrorNotSupported if n too large
+cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
+                           long long ldq, int j, const double* w_in, double* partials,
+                           double* h_out);
 
 }  // namespace ocp
