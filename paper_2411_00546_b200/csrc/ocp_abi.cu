@@ -173,7 +173,6 @@ double band_lu_flops(long long N, long long w) {
   return tot;
 }
 
-int lu_smem_bytes(int W) { return (NB * (NB + W + 1) + NB * W + 2 * NB * NB) * (int)sizeof(double); }
 
 int upload_list(ocp_ctx* ctx, const std::vector<int>& list) {
   std::copy(list.begin(), list.end(), ctx->h_list);
@@ -189,7 +188,7 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   for (int i : list) flops += ctx->sub_flops[i];
   Timer t(ctx, CLS_FACTOR, flops);
   const int grid = std::min(cnt, ctx->lu_grid);
-  k_band_factor<<<grid, LU_THREADS, lu_smem_bytes(ctx->maxW), ctx->stream>>>(
+  k_band_factor<<<grid, LU_THREADS, factor_smem_bytes(ctx->maxW), ctx->stream>>>(
       ctx->d_subs, d_list, cnt, ctx->P, ctx->JD, fac, ctx->scratch, ctx->ws_stride, ctx->d_status);
   CKL();
   return OCP_OK;
@@ -283,7 +282,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       s.w = 2 * s.nc;
       s.W = ((s.w + NB - 1) / NB) * NB;
       s.N = 2 * R * C;
-      s.NP = ((s.N + NB - 1) / NB) * NB;
+      s.NP = ((s.N + NBF - 1) / NBF) * NBF;
       s.loc = loc;
       s.fac = fac;
       s.ref = ref;
@@ -302,7 +301,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->pool_len = loc;
   ctx->fac_len = fac;
   ctx->ref_len = ref;
-  ctx->maxWS = ctx->maxW + NB;
+  ctx->maxWS = ctx->maxW + NBF;
   if (ctx->maxW > MAX_W) {
     int code = fail(nullptr, OCP_ERR_UNSUPPORTED,
                     "local half-bandwidth %d exceeds the compiled limit %d", ctx->maxW, MAX_W);
@@ -375,12 +374,12 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     CKC(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa;
     CKC(cudaFuncGetAttributes(&fa, k_band_factor));
-    if (lu_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
+    if (factor_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
       fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
       return cleanup_fail(OCP_ERR_UNSUPPORTED);
     }
     CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             lu_smem_bytes(ctx->maxW)));
+                             factor_smem_bytes(ctx->maxW)));
     const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
     if (solve_smem > optin) {
       fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");

@@ -33,6 +33,7 @@ __global__ void k_gemv_add(long long n, const double* Q, long long ldq, int k, c
                            const double* x, double* out);
 __global__ void k_recover_control(long long n, Phys P, const double* p, double eps, double* u);
 
+int factor_smem_bytes(int W);
 __global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
                               const double* JDpool, double* fac_pool, double* scratch,
                               long long ws_stride, int* status);
