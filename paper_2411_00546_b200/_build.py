@@ -44,7 +44,8 @@ def stale():
 def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", LIB] + sources()
+    extra = ["-DOCP_PHASE_TIMING"] if os.environ.get("OCP_PHASE_TIMING") else []
+    cmd = [nvcc()] + NVCC_FLAGS + extra + ["-o", LIB] + sources()
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=CSRC)

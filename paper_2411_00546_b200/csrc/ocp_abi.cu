@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,7 @@
 #include "ocp_kernels.cuh"
 
 using namespace ocp;
+namespace ocp { void read_phase(unsigned long long* out); }
 
 namespace {
 
@@ -353,7 +355,11 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     CKC(cudaMemcpy(ctx->d_list_all, all.data(), I * sizeof(int), cudaMemcpyHostToDevice));
   }
   // LU windows: up to 2 CTAs per SM, one (W+NB)^2 window each (L2 resident)
-  ctx->lu_grid = std::min(I, 2 * ctx->num_sms);
+  {
+    int per_sm = 2;
+    if (const char* e = getenv("OCP_LU_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));
+    ctx->lu_grid = std::min(I, per_sm * ctx->num_sms);
+  }
   ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
   CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
   CKC(cudaMalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
@@ -900,6 +906,10 @@ int ocp_reset_stats(ocp_ctx* ctx) {
   ctx->stat_flops = ctx->stat_bytes = ctx->stat_dof = 0;
   return OCP_OK;
 }
+
+#ifdef OCP_PHASE_TIMING
+int ocp_debug_phase(unsigned long long* out) { ocp::read_phase(out); return 0; }
+#endif
 
 int ocp_event_record(ocp_ctx* ctx, int slot) {
   if (!ctx || slot < 0 || slot >= 16) return OCP_ERR_ARG;

@@ -13,9 +13,8 @@
 // subdomain (persistent over the work list, 2 CTAs per SM).  Per panel:
 //   1. panel (W+32 rows x 32) and U row block (32 x W) -> shared memory;
 //   2. the 32x32 diagonal block in two 16x16 levels: a single warp factors a
-//      16x16 block in registers (shuffles, no block barrier) and replaces it
-//      by its packed triangular inverses; everything else is products with
-//      those inverses, all threads in parallel:
+//      16x16 block in registers (shuffles, no block barrier); the rest are
+//      independent 16-wide triangular solves, all threads in parallel:
 //        LU(A_aa);  U_ab = La^-1 A_ab, L_ba = A_ba Ua^-1, X_a = A21_a Ua^-1,
 //        Y_a = La^-1 A12_a;  S = A_bb - L_ba U_ab, LU(S)  (warp 0) while the
 //        other warps form A21_b - X_a U_ab and A12_b - L_ba Y_a;  then
@@ -24,8 +23,11 @@
 //      (DMMA m8n8k4, 16x16 warp tiles; measured 37.1 TFLOP/s vs 34.2 for
 //      DFMA on this B200, tools/dmma_peak.cu); the window is a circular
 //      (W+32)^2 buffer in a per-CTA global scratch that stays L2-resident
-//      (0.5 B of L2 traffic per FMA), plus the streaming of the two finished
-//      16-blocks to the factor store and the matrix entries entering the window.
+//      (0.5 B of L2 traffic per FMA).  Entries no panel has updated yet are
+//      never stored: they are generated from the Jacobian diagonals where
+//      they are first read.  One warp forms the 16x16 triangular inverses the
+//      solve kernel uses (off the serial path), then all warps stream the
+//      finished 16-blocks to the factor store.
 //
 // Factor store, per 16-block K (the unit the solve kernel streams):
 //   [L: 16 x (W+1)  L[k0+c+1+s][k0+c], s < W][U: 16 x (W+1)  U[k0+c][k0+c+s]]
@@ -36,6 +38,22 @@
 
 namespace ocp {
 
+// optional per-phase cycle counters (build with -DOCP_PHASE_TIMING; tools/phase_dbg.py)
+#ifdef OCP_PHASE_TIMING
+__device__ unsigned long long g_phase[8];
+#define PHASE_START() long long t_last = clock64()
+#define PHASE_MARK(k)                                                                   \
+  do {                                                                                  \
+    if (tid == 0) {                                                                     \
+      const long long now = clock64();                                                  \
+      atomicAdd(&g_phase[k], (unsigned long long)(now - t_last));                       \
+      t_last = now;                                                                     \
+    }                                                                                   \
+  } while (0)
+#else
+#define PHASE_START() (void)0
+#define PHASE_MARK(k) (void)0
+#endif
 constexpr int LDP = NBF + 4; // panel row stride, = 4 (mod 16): conflict-free DMMA A fragments
 
 // original Jacobian entry (i, j) of the padded band-ordered local system
@@ -77,34 +95,79 @@ __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 
-// One warp: factor the 16x16 block at P[(o+i)*LDP + o+j] (no pivoting) and
-// replace it by its packed inverses: strict lower part = (L^-1) (unit
-// diagonal implied), upper part incl. diagonal = U^-1.
-__device__ __forceinline__ void warp_lu16_inverse(double* P, int o, int lane, int* bad) {
+// Reciprocal without the IEEE slow path (no call => nothing spills around it):
+// MUFU seed + two Newton steps, ~1 ulp; pivots here are O(1/h^2) normal numbers.
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// One warp factors the 16x16 block at P[(o+i)*LDP + o+j] in place (no
+// pivoting; L strict lower, U upper) and stores 1/U[i][i] in rd[i].
+// Shared-memory right-looking form: lane r < 16 owns row r, the pivot row is
+// read as a broadcast; no shuffles (their diverged-warp slow path cost 17x
+// inside this kernel).
+__device__ __forceinline__ void warp_lu16(double* P, int o, int lane, double* rd, int* bad) {
+  __syncwarp();
   const int r = lane & 15;
+  double* prow = P + (o + r) * LDP + o;
+#pragma unroll 1
+  for (int c = 0; c < 16; ++c) {
+    const double* pc = P + (o + c) * LDP + o;
+    const double piv = pc[c];
+    const double rp = fast_rcp(piv);
+    if (lane == 0) {
+      rd[c] = rp;
+      if (!(piv != 0.0 && isfinite(piv))) *bad = 1;
+    }
+    if (lane < 16 && r > c) {
+      const double l = prow[c] * rp;
+      prow[c] = l;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j > c) prow[j] = fma(-l, pc[j], prow[j]);
+    }
+    __syncwarp();
+  }
+}
+
+// row task: x U = a for the upper factor U at P block (o, o), in place on row[0..16)
+__device__ __forceinline__ void row_solve_u(double* row, const double* P, int o, const double* rd) {
   double a[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = P[(o + r) * LDP + o + j];
+  for (int k = 0; k < 16; ++k) a[k] = row[k];
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    const double piv = __shfl_sync(0xffffffffu, a[c], c);
-    if (lane == 0 && !(piv != 0.0 && isfinite(piv))) *bad = 1;
-    const double l = a[c] / piv;
+    a[c] *= rd[c];
 #pragma unroll
-    for (int j = c + 1; j < 16; ++j) {
-      const double pj = __shfl_sync(0xffffffffu, a[j], c);
-      if (r > c) a[j] = fma(-l, pj, a[j]);
-    }
-    if (r > c) a[c] = l;
+    for (int j = c + 1; j < 16; ++j) a[j] = fma(-a[c], P[(o + c) * LDP + o + j], a[j]);
   }
-  if (lane < 16) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) P[(o + r) * LDP + o + j] = a[j];
-  }
-  __syncwarp();
-  // column j of L^-1 (lanes 0..15) or of U^-1 (lanes 16..31)
+  for (int k = 0; k < 16; ++k) row[k] = a[k];
+}
+
+// column task: L y = a for the unit lower factor L at P block (o, o), in place on col[t*ld]
+__device__ __forceinline__ void col_solve_l(double* col, int ld, const double* P, int o) {
+  double a[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) a[t] = col[t * ld];
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+#pragma unroll
+    for (int t = k + 1; t < 16; ++t) a[t] = fma(-P[(o + t) * LDP + o + k], a[k], a[t]);
+#pragma unroll
+  for (int t = 0; t < 16; ++t) col[t * ld] = a[t];
+}
+
+// lane j < 16: column j of the unit-lower inverse of L at block (o, o);
+// lane 16 + j: column j of the inverse of U.  Result entry i in x[i].
+__device__ __forceinline__ void tri_inverse_lane(const double* P, int o, int lane, const double* rd,
+                                                 double* x) {
   const int j = lane & 15;
-  double x[16];
   if (lane < 16) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -119,46 +182,8 @@ __device__ __forceinline__ void warp_lu16_inverse(double* P, int o, int lane, in
       double acc = (i == j) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = i + 1; k < 16; ++k) acc = fma(-P[(o + i) * LDP + o + k], x[k], acc);
-      x[i] = i <= j ? acc / P[(o + i) * LDP + o + i] : 0.0;
+      x[i] = i <= j ? acc * rd[i] : 0.0;
     }
-  }
-  __syncwarp();
-  if (lane < 16) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i > j) P[(o + i) * LDP + o + j] = x[i];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i <= j) P[(o + i) * LDP + o + j] = x[i];
-  }
-}
-
-// row task: out[0..16) = a[0..16) U^-1, U^-1 packed in the upper part of P block (o, o)
-__device__ __forceinline__ void row_times_uinv(double* row, const double* P, int o) {
-  double a[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) a[k] = row[k];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    double acc = 0.0;
-#pragma unroll
-    for (int k = 0; k <= c; ++k) acc = fma(a[k], P[(o + k) * LDP + o + c], acc);
-    row[c] = acc;
-  }
-}
-
-// column task: out[t*ld] = (L^-1 a)[t], L^-1 packed in the strict lower part of P block (o, o)
-__device__ __forceinline__ void linv_times_col(double* col, int ld, const double* P, int o) {
-  double a[16];
-#pragma unroll
-  for (int t = 0; t < 16; ++t) a[t] = col[t * ld];
-#pragma unroll
-  for (int t = 15; t >= 0; --t) {
-    double acc = a[t];
-#pragma unroll
-    for (int k = 0; k < t; ++k) acc = fma(P[(o + t) * LDP + o + k], a[k], acc);
-    col[t * ld] = acc;
   }
 }
 
@@ -167,7 +192,10 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
               double* fac_pool, double* scratch, long long ws_stride, int* status) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int bad;
+  __shared__ double rd[2][16];  // reciprocal pivots of U_aa, U_cc
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = LU_THREADS / 32;
+  constexpr int SIDE = NW - 1;  // forms the block inverses at the start of the update phase
   double* win = scratch + (long long)blockIdx.x * ws_stride;
   for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
     const int sid = list[li];
@@ -179,63 +207,69 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
     double* P = sm;                          // P[r*LDP + c]: panel row k0+r, column k0+c
     double* U = P + (W + NBF) * LDP;         // U[t*LDU + c]: U12 row k0+t, column k0+32+c
     if (tid == 0) bad = 0;
-    // initial window [0, WS)^2
-    for (int i = warp; i < WS; i += LU_THREADS / 32) {
-      const RowInfo r = row_info(s, JD, i);
-      for (int j = lane; j < WS; j += 32) win[(long long)i * WS + j] = entry(s, r, j, off);
-    }
     __syncthreads();
     const int nblk = NP / NBF;
     int ks = 0;  // k0 mod WS
     for (int K = 0; K < nblk; ++K) {
       const int k0 = K * NBF;
-      // ---- 1. panel + U row block -> shared (warp per row, lanes along columns)
+      PHASE_START();
+      // ---- 1. panel + U row block -> shared (warp per row, lanes along columns).
+      //         An entry (i, j) has been touched by an earlier panel update iff
+      //         K > 0 and max(i, j) < k0 + W; all others still hold their
+      //         original value and are generated here instead of stored.
       {
+        const int fresh = K == 0 ? k0 : k0 + W;   // indices >= fresh are untouched
         int pcol = ks + lane; pcol -= pcol >= WS ? WS : 0;
-        for (int r = warp; r < W + NBF; r += 2 * (LU_THREADS / 32)) {
-          int pr0 = ks + r; pr0 -= pr0 >= WS ? WS : 0; pr0 -= pr0 >= WS ? WS : 0;
-          const int r1 = r + LU_THREADS / 32;
-          int pr1 = ks + r1; pr1 -= pr1 >= WS ? WS : 0; pr1 -= pr1 >= WS ? WS : 0;
-          const double v0 = win[(long long)pr0 * WS + pcol];
-          const double v1 = r1 < W + NBF ? win[(long long)pr1 * WS + pcol] : 0.0;
-          P[r * LDP + lane] = v0;
-          if (r1 < W + NBF) P[r1 * LDP + lane] = v1;
+        for (int r = warp; r < W + NBF; r += NW) {
+          const int i = k0 + r;
+          double v;
+          if (i >= fresh || k0 + lane >= fresh) {
+            v = entry(s, row_info(s, JD, i), k0 + lane, off);
+          } else {
+            int pr = ks + r; pr -= pr >= WS ? WS : 0; pr -= pr >= WS ? WS : 0;
+            v = win[(long long)pr * WS + pcol];
+          }
+          P[r * LDP + lane] = v;
         }
-        for (int t = warp; t < NBF; t += LU_THREADS / 32) {
+        for (int t = warp; t < NBF; t += NW) {
+          const int i = k0 + t;
           int pr = ks + t; pr -= pr >= WS ? WS : 0;
           const double* src = win + (long long)pr * WS;
+          const RowInfo ri = row_info(s, JD, i);
           double v[8];
-          int nv = 0;
+          int pc = ks + NBF + lane; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int c = lane + 32 * q;
-            if (c < W) {
-              int pc = ks + NBF + c; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
-              v[q] = src[pc];
-              nv = q + 1;
-            }
+            const int c = lane + 32 * q, j = k0 + NBF + c;
+            v[q] = c >= W ? 0.0 : (j >= fresh || i >= fresh) ? entry(s, ri, j, off) : src[pc];
+            pc += 32;
+            pc -= pc >= WS ? WS : 0;
           }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            if (q < nv) U[t * LDU + lane + 32 * q] = v[q];
+            if (lane + 32 * q < W) U[t * LDU + lane + 32 * q] = v[q];
         }
       }
       __syncthreads();
-      // ---- 2a. LU(A_aa) and its inverses (warp 0)
-      if (warp == 0) warp_lu16_inverse(P, 0, lane, &bad);
+      PHASE_MARK(1);
+      // ---- 2a. LU(A_aa) (warp 0)
+      if (warp == 0) warp_lu16(P, 0, lane, rd[0], &bad);
       __syncthreads();
-      // ---- 2b. rows 16..W+31, cols 0..15: times Ua^-1  (L_ba and X_a)
-      //          cols: P[0..16)[16..32) and U[0..16)[*]: La^-1 times  (U_ab and Y_a)
+      PHASE_MARK(2);
+      // ---- 2b. L_ba, X_a (rows 16..W+31, cols 0..15) solve against U_aa;
+      //          U_ab (rows 0..15, cols 16..31), Y_a (U rows 0..15) against L_aa
       for (int task = tid; task < 2 * (W + 16); task += LU_THREADS) {
-        if (task < W + 16) row_times_uinv(P + (16 + task) * LDP, P, 0);
-        else {
+        if (task < W + 16) {
+          row_solve_u(P + (16 + task) * LDP, P, 0, rd[0]);
+        } else {
           const int c = task - (W + 16);
-          if (c < 16) linv_times_col(P + 16 + c, LDP, P, 0);
-          else linv_times_col(U + (c - 16), LDU, P, 0);
+          if (c < 16) col_solve_l(P + 16 + c, LDP, P, 0);
+          else col_solve_l(U + (c - 16), LDU, P, 0);
         }
       }
       __syncthreads();
-      // ---- 2c. warp 0: S = A_bb - L_ba U_ab, LU(S) + inverses;
+      PHASE_MARK(3);
+      // ---- 2c. warp 0: S = A_bb - L_ba U_ab, LU(S);
       //          warps 1..7: A21_b -= X_a U_ab (rows 32..), A12_b -= L_ba Y_a
       if (warp == 0) {
         if (lane < 16) {
@@ -253,7 +287,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
           for (int j = 0; j < 16; ++j) row[j] = a[j];
         }
         __syncwarp();
-        warp_lu16_inverse(P, 16, lane, &bad);
+        warp_lu16(P, 16, lane, rd[1], &bad);
       } else {
         for (int task = tid - 32; task < 2 * W; task += LU_THREADS - 32) {
           if (task < W) {  // row 32+task: cols 16..31 -= X_a[row] U_ab
@@ -285,20 +319,46 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
         }
       }
       __syncthreads();
-      // ---- 2d. X_b = (.) Uc^-1 (rows 32..), Y_b = Lc^-1 (.) (U rows 16..31)
+      PHASE_MARK(4);
+      // ---- 2d. X_b solve against U_cc (rows 32..), Y_b against L_cc (U rows 16..31)
       for (int task = tid; task < 2 * W; task += LU_THREADS) {
-        if (task < W) row_times_uinv(P + (NBF + task) * LDP + 16, P, 16);
-        else linv_times_col(U + 16 * LDU + (task - W), LDU, P, 16);
+        if (task < W) row_solve_u(P + (NBF + task) * LDP + 16, P, 16, rd[1]);
+        else col_solve_l(U + 16 * LDU + (task - W), LDU, P, 16);
       }
       __syncthreads();
-      // ---- 3a. rank-32 trailing update on [k0+32, k0+32+W)^2 with DMMA
+      PHASE_MARK(5);
+      // ---- 3a. side warp first forms the 16x16 triangular inverses of the two
+      //          diagonal blocks and writes them into the factor store
+      if (warp == SIDE) {
+#pragma unroll 1
+        for (int b = 0; b < 2; ++b) {
+          double x[16];
+          tri_inverse_lane(P, 16 * b, lane, rd[b], x);
+          double* Lb = fac + (long long)(2 * K + b) * 2 * NB * LD;
+          double* Ub = Lb + NB * LD;
+          const int j = lane & 15;
+          if (lane < 16) {   // L^-1 column j: rows i > j -> Lb[j][i - j - 1]
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i > j) Lb[j * LD + i - j - 1] = x[i];
+          } else {           // U^-1 column j: rows i <= j -> Ub[i][j - i]
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i <= j) Ub[i * LD + j - i] = x[i];
+          }
+        }
+      }
+      // ---- 3b. rank-32 trailing update on [k0+32, k0+32+W)^2 with DMMA
       {
         const int TW = W >> 4, g = lane >> 2, t4 = lane & 3;
-        for (int wt = warp; wt < TW * TW; wt += LU_THREADS / 32) {
+        for (int wt = (warp + 1) & (NW - 1); wt < TW * TW; wt += NW) {
           const int tr = wt / TW, tc = wt - tr * TW;
           const int R0 = 16 * tr, C0 = 16 * tc;
           double c[2][2][2];
           long long addr[2][2];
+          // the last 32 rows/columns of the window (and all of it in panel 0)
+          // have never been updated: generated, not loaded
+          const bool gen = K == 0 || R0 + 16 > W - NBF || C0 + 16 > W - NBF;
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
             int pr = ks + NBF + R0 + 8 * mi + g; pr -= pr >= WS ? WS : 0; pr -= pr >= WS ? WS : 0;
@@ -306,9 +366,27 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
             for (int ni = 0; ni < 2; ++ni) {
               int pc = ks + NBF + C0 + 8 * ni + 2 * t4; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
               addr[mi][ni] = (long long)pr * WS + pc;
-              const double2 v = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
-              c[mi][ni][0] = v.x;
-              c[mi][ni][1] = v.y;
+              if (!gen) {
+                const double2 v = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
+                c[mi][ni][0] = v.x;
+                c[mi][ni][1] = v.y;
+              } else {
+                const int i = k0 + NBF + R0 + 8 * mi + g, j = k0 + NBF + C0 + 8 * ni + 2 * t4;
+                const int fresh = K == 0 ? k0 : k0 + W;
+                double v0, v1;
+                if (i >= fresh || j + 1 >= fresh) {
+                  const RowInfo ri = row_info(s, JD, i);
+                  const double2 w = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
+                  v0 = (i >= fresh || j >= fresh) ? entry(s, ri, j, off) : w.x;
+                  v1 = entry(s, ri, j + 1, off);
+                } else {
+                  const double2 w = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
+                  v0 = w.x;
+                  v1 = w.y;
+                }
+                c[mi][ni][0] = v0;
+                c[mi][ni][1] = v1;
+              }
             }
           }
           const double* ap = P + (NBF + R0 + g) * LDP + t4;
@@ -329,46 +407,22 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
               *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
         }
       }
-      // ---- 3b. stream the two finished 16-blocks to the factor store
-      //          (the in-block triangles are the packed inverses in P)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
+      // ---- 3c. the rest of the two finished 16-blocks -> factor store
+      for (int rowid = warp; rowid < 2 * NB; rowid += NW) {
+        const int b = rowid >> 4, c = rowid & 15, o = 16 * b;
         double* Lb = fac + (long long)(2 * K + b) * 2 * NB * LD;
         double* Ub = Lb + NB * LD;
-        const int o = 16 * b;
-        for (int c = warp; c < NB; c += LU_THREADS / 32) {
-          for (int sidx = lane; sidx < LD; sidx += 32) {
-            // L column o+c: rows o+c+1+sidx (inverse entries inside the block)
-            Lb[c * LD + sidx] = sidx == W ? 0.0 : P[(o + c + 1 + sidx) * LDP + o + c];
-            const int col = o + c + sidx;
-            Ub[c * LD + sidx] = col < NBF ? P[(o + c) * LDP + col] : U[(o + c) * LDU + col - NBF];
-          }
-        }
-      }
-      // ---- 3c. entries entering the window for panel K+1 (slots of panel K)
-      {
-        const int base = k0 + NBF + W;             // first new index
-        const int band = 2 * s.nc;
-        for (int t = warp; t < NBF; t += LU_THREADS / 32) {  // new rows
-          const RowInfo r = row_info(s, JD, base + t);
-          int prow = ks + t; prow -= prow >= WS ? WS : 0;
-          double* dst = win + (long long)prow * WS;
-          for (int c = lane; c < W + NBF; c += 32) {
-            int pc = ks + NBF + c; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
-            const int j = k0 + NBF + c, d = j - r.i;
-            dst[pc] = (d > band || d < -band) ? 0.0 : entry(s, r, j, off);
-          }
-        }
-        for (int rr = warp; rr < W; rr += LU_THREADS / 32) {  // new columns
-          const int i = k0 + NBF + rr, j = base + lane, d = j - i;
-          int pr = ks + NBF + rr; pr -= pr >= WS ? WS : 0; pr -= pr >= WS ? WS : 0;
-          int pcol = ks + lane; pcol -= pcol >= WS ? WS : 0;
-          double v = 0.0;
-          if (d <= band) v = entry(s, row_info(s, JD, i), j, off);
-          win[(long long)pr * WS + pcol] = v;
+        const int lfirst = NB - 1 - c;   // first L entry outside the block
+        for (int sidx = lfirst + lane; sidx < LD; sidx += 32)
+          Lb[c * LD + sidx] = sidx == W ? 0.0 : P[(o + c + 1 + sidx) * LDP + o + c];
+        const int ufirst = NB - c;       // first U entry outside the block
+        for (int sidx = ufirst + lane; sidx < LD; sidx += 32) {
+          const int col = o + c + sidx;
+          Ub[c * LD + sidx] = col < NBF ? P[(o + c) * LDP + col] : U[(o + c) * LDU + col - NBF];
         }
       }
       __syncthreads();
+      PHASE_MARK(6);
       if (bad) break;
       ks += NBF;
       ks -= ks >= WS ? WS : 0;
@@ -378,6 +432,9 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
   }
 }
 
+#ifdef OCP_PHASE_TIMING
+void read_phase(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_phase, 8 * sizeof(unsigned long long)); }
+#endif
 int factor_smem_bytes(int W) {
   return (int)sizeof(double) * ((W + NBF) * LDP + NBF * (W + 4));
 }
