@@ -52,5 +52,20 @@ def build(force=False, verbose=False):
     return LIB
 
 
+TOOLS = {"fp64_peak": "fp64_peak.cu", "dmma_peak": "dmma_peak.cu"}
+
+
+def build_tools(verbose=False):
+    """Peak probes used by bench.py for the FP64 roofline denominator."""
+    tdir = os.path.join(os.path.dirname(HERE), "tools")
+    for exe, src in TOOLS.items():
+        cmd = [nvcc(), "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
+               os.path.join(tdir, exe), os.path.join(tdir, src)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    build_tools(verbose=True)

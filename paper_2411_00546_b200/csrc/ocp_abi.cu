@@ -43,7 +43,8 @@ struct ocp_ctx {
   Phys P{};
   std::vector<SubInfo> subs;
   std::vector<double> sub_flops;    // algorithmic band-LU flops per subdomain
-  std::vector<double> sub_fbytes;   // algorithmic factor bytes per subdomain
+  std::vector<double> sub_fbytes;   // algorithmic factor bytes of a full solve per subdomain
+  std::vector<double> sub_jbytes;   // algorithmic factor bytes of a JVP solve (owned rows only)
   std::vector<long long> sub_dofs;  // 2 R C
   SubInfo* d_subs = nullptr;
   long long pool_len = 0, fac_len = 0, ref_len = 0, dof_total = 0;
@@ -294,6 +295,13 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       ctx->subs.push_back(s);
       ctx->sub_flops.push_back(band_lu_flops(s.N, s.w));
       ctx->sub_fbytes.push_back(8.0 * (double)s.N * (2.0 * s.w + 1.0));
+      {
+        // the JVP needs x only on the ownership block: the backward sweep
+        // stops at its first oriented row (k_band_solve MODE 1)
+        const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+        const double kstop = 2.0 * s.nc * a_own;
+        ctx->sub_jbytes.push_back(8.0 * ((double)s.N * s.w + ((double)s.N - kstop) * (s.w + 1.0)));
+      }
       ctx->sub_dofs.push_back(s.N);
       ctx->maxW = std::max(ctx->maxW, s.W);
       ctx->maxNP = std::max(ctx->maxNP, s.NP);
@@ -666,7 +674,7 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
   CKL();
   {
     double bytes = 0;
-    for (int i = 0; i < I; ++i) bytes += ctx->sub_fbytes[i];
+    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
     Timer t(ctx, CLS_SOLVE, 0, bytes);
     CK(launch_band_solve(1, I, st, ctx->d_subs, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B,
                          ctx->maxW));
