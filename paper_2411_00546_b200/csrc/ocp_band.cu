@@ -340,11 +340,11 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
           if (lane < 16) {   // L^-1 column j: rows i > j -> Lb[j][i - j - 1]
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (i > j) Lb[j * LD + i - j - 1] = x[i];
+              if (i > j) __stcs(Lb + j * LD + i - j - 1, x[i]);
           } else {           // U^-1 column j: rows i <= j -> Ub[i][j - i]
 #pragma unroll
             for (int i = 0; i < 16; ++i)
-              if (i <= j) Ub[i * LD + j - i] = x[i];
+              if (i <= j) __stcs(Ub + i * LD + j - i, x[i]);
           }
         }
       }
@@ -408,17 +408,18 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
         }
       }
       // ---- 3c. the rest of the two finished 16-blocks -> factor store
+      //          (streaming stores: the 8 GB store must not evict the L2-resident windows)
       for (int rowid = warp; rowid < 2 * NB; rowid += NW) {
         const int b = rowid >> 4, c = rowid & 15, o = 16 * b;
         double* Lb = fac + (long long)(2 * K + b) * 2 * NB * LD;
         double* Ub = Lb + NB * LD;
         const int lfirst = NB - 1 - c;   // first L entry outside the block
         for (int sidx = lfirst + lane; sidx < LD; sidx += 32)
-          Lb[c * LD + sidx] = sidx == W ? 0.0 : P[(o + c + 1 + sidx) * LDP + o + c];
+          __stcs(Lb + c * LD + sidx, sidx == W ? 0.0 : P[(o + c + 1 + sidx) * LDP + o + c]);
         const int ufirst = NB - c;       // first U entry outside the block
         for (int sidx = ufirst + lane; sidx < LD; sidx += 32) {
           const int col = o + c + sidx;
-          Ub[c * LD + sidx] = col < NBF ? P[(o + c) * LDP + col] : U[(o + c) * LDU + col - NBF];
+          __stcs(Ub + c * LD + sidx, col < NBF ? P[(o + c) * LDP + col] : U[(o + c) * LDU + col - NBF]);
         }
       }
       __syncthreads();
