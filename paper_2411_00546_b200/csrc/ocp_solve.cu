@@ -135,16 +135,17 @@ k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const
       const int r = k0 + NB + t;
       if (t < W && r < NP) {
         const double* lp = Lb + (NB - 1) + t;        // column c entry at lp + c * (LD - 1)
-        double acc = ring[r & RM];
+        // four independent accumulators: the 16-term dot is latency-bound otherwise
+        double acc[4] = {ring[r & RM], 0.0, 0.0, 0.0};
         if (t + NB <= W) {
 #pragma unroll
-          for (int c = 0; c < NB; ++c) acc = fma(-lp[c * (LD - 1)], ys[c], acc);
+          for (int c = 0; c < NB; ++c) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
         } else {
 #pragma unroll
           for (int c = 0; c < NB; ++c)
-            if (NB - 1 + t - c < W) acc = fma(-lp[c * (LD - 1)], ys[c], acc);
+            if (NB - 1 + t - c < W) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
         }
-        ring[r & RM] = acc;
+        ring[r & RM] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
     }
     __syncthreads();
@@ -184,14 +185,16 @@ k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const
     const double* Ub = stage + st * SB;
     mbar_wait(&ubars[st], (step / SOLVE_STAGES) & 1);
     {  // r_c = z_c - U12 x   (row gi, lanes gj stride 16 over the band)
-      double acc = 0.0;
+      double acc0 = 0.0, acc1 = 0.0;
       const double* up = Ub + gi * LD;
       const int base = k0 + gi;
 #pragma unroll 4
-      for (int m = 0; m < MW; ++m) {
+      for (int m = 0; m < MW; m += 2) {
         const int sidx = NB - gi + gj + 16 * m;
-        if (sidx <= W) acc = fma(up[sidx], ring[(base + sidx) & RM], acc);
+        if (sidx <= W) acc0 = fma(up[sidx], ring[(base + sidx) & RM], acc0);
+        if (sidx + 16 <= W) acc1 = fma(up[sidx + 16], ring[(base + sidx + 16) & RM], acc1);
       }
+      double acc = acc0 + acc1;
 #pragma unroll
       for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (gj == 0) ys[gi] = ring[(k0 + gi) & RM] - acc;
