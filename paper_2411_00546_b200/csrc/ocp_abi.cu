@@ -283,7 +283,9 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       s.nr = std::max(R, C);
       s.nc = std::min(R, C);
       s.w = 2 * s.nc;
-      s.W = ((s.w + NB - 1) / NB) * NB;
+      // padded half-bandwidth: a multiple of 16, and at least one factor block
+      // (the 32x32 in-block inverses are stored inside the band columns)
+      s.W = std::max(((s.w + NB - 1) / NB) * NB, NBF);
       s.N = 2 * R * C;
       s.NP = ((s.N + NBF - 1) / NBF) * NBF;
       s.loc = loc;

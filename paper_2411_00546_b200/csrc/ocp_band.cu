@@ -29,10 +29,10 @@
 //      solve kernel uses (off the serial path), then all warps stream the
 //      finished 16-blocks to the factor store.
 //
-// Factor store, per 16-block K (the unit the solve kernel streams):
-//   [L: 16 x (W+1)  L[k0+c+1+s][k0+c], s < W][U: 16 x (W+1)  U[k0+c][k0+c+s]]
+// Factor store, per 32-block K (the unit the solve kernel streams):
+//   [L: 32 x (W+1)  L[k0+c+1+s][k0+c], s < W][U: 32 x (W+1)  U[k0+c][k0+c+s]]
 // with the in-block triangles replaced by their inverses: L entries with
-// c+1+s < 16 hold (L11^{-1})[c+1+s][c], U entries with c+s < 16 hold
+// c+1+s < 32 hold (L11^{-1})[c+1+s][c], U entries with c+s < 32 hold
 // (U11^{-1})[c][c+s].
 #include "ocp_kernels.cuh"
 
@@ -327,25 +327,62 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       }
       __syncthreads();
       PHASE_MARK(5);
-      // ---- 3a. side warp first forms the 16x16 triangular inverses of the two
-      //          diagonal blocks and writes them into the factor store
+      // ---- 3a. side warp: the 32x32 inverses of L11 and U11 (the solve kernel
+      //          applies them as mat-vecs), written in place of the in-block
+      //          triangles of the factor store:
+      //            L11^-1 = [[La^-1, 0], [X, Lc^-1]],  X = -Lc^-1 L_ba La^-1
+      //            U11^-1 = [[Ua^-1, Y], [0, Uc^-1]],  Y = -Ua^-1 U_ab Uc^-1
       if (warp == SIDE) {
-#pragma unroll 1
-        for (int b = 0; b < 2; ++b) {
-          double x[16];
-          tri_inverse_lane(P, 16 * b, lane, rd[b], x);
-          double* Lb = fac + (long long)(2 * K + b) * 2 * NB * LD;
-          double* Ub = Lb + NB * LD;
-          const int j = lane & 15;
-          if (lane < 16) {   // L^-1 column j: rows i > j -> Lb[j][i - j - 1]
+        double* Lb = fac + (long long)K * 2 * NBF * LD;
+        double* Ub = Lb + NBF * LD;
+        const int j = lane & 15;
+        double x[16], z[16];
+        tri_inverse_lane(P, 0, lane, rd[0], x);    // La^-1 / Ua^-1 column j
+        tri_inverse_lane(P, 16, lane, rd[1], z);   // Lc^-1 / Uc^-1 column j
+        if (lane < 16) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i > j) __stcs(Lb + j * LD + i - j - 1, x[i]);
-          } else {           // U^-1 column j: rows i <= j -> Ub[i][j - i]
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i <= j) __stcs(Ub + i * LD + j - i, x[i]);
+          for (int i = 0; i < 16; ++i) {
+            if (i > j) __stcs(Lb + j * LD + i - j - 1, x[i]);                 // La^-1
+            if (i > j) __stcs(Lb + (16 + j) * LD + i - j - 1, z[i]);          // Lc^-1
           }
+          // X[:, j] = Lc^-1 (-L_ba La^-1[:, j]): forward substitution with unit Lc
+          double t[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc = fma(-P[(16 + i) * LDP + k], x[k], acc);
+            t[i] = acc;
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+#pragma unroll
+            for (int i = k + 1; i < 16; ++i) t[i] = fma(-P[(16 + i) * LDP + 16 + k], t[k], t[i]);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) __stcs(Lb + j * LD + (16 + i) - j - 1, t[i]);   // X[i][j]
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i <= j) __stcs(Ub + i * LD + j - i, x[i]);                    // Ua^-1
+            if (i <= j) __stcs(Ub + (16 + i) * LD + j - i, z[i]);             // Uc^-1
+          }
+          // Y[:, j] = Ua^-1 (-U_ab Uc^-1[:, j]): back substitution with Ua
+          double t[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) acc = fma(-P[i * LDP + 16 + k], z[k], acc);
+            t[i] = acc;
+          }
+#pragma unroll
+          for (int k = 15; k >= 0; --k) {
+            t[k] *= rd[0][k];
+#pragma unroll
+            for (int i = 0; i < k; ++i) t[i] = fma(-P[i * LDP + k], t[k], t[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) __stcs(Ub + i * LD + (16 + j) - i, t[i]);   // Y[i][j]
         }
       }
       // ---- 3b. rank-32 trailing update on [k0+32, k0+32+W)^2 with DMMA
@@ -407,20 +444,17 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
               *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
         }
       }
-      // ---- 3c. the rest of the two finished 16-blocks -> factor store
+      // ---- 3c. the rest of the finished 32-block -> factor store
       //          (streaming stores: the 8 GB store must not evict the L2-resident windows)
-      for (int rowid = warp; rowid < 2 * NB; rowid += NW) {
-        const int b = rowid >> 4, c = rowid & 15, o = 16 * b;
-        double* Lb = fac + (long long)(2 * K + b) * 2 * NB * LD;
-        double* Ub = Lb + NB * LD;
-        const int lfirst = NB - 1 - c;   // first L entry outside the block
+      for (int c = warp; c < NBF; c += NW) {
+        double* Lb = fac + (long long)K * 2 * NBF * LD;
+        double* Ub = Lb + NBF * LD;
+        const int lfirst = NBF - 1 - c;  // first L entry below the block
         for (int sidx = lfirst + lane; sidx < LD; sidx += 32)
-          __stcs(Lb + c * LD + sidx, sidx == W ? 0.0 : P[(o + c + 1 + sidx) * LDP + o + c]);
-        const int ufirst = NB - c;       // first U entry outside the block
-        for (int sidx = ufirst + lane; sidx < LD; sidx += 32) {
-          const int col = o + c + sidx;
-          __stcs(Ub + c * LD + sidx, col < NBF ? P[(o + c) * LDP + col] : U[(o + c) * LDU + col - NBF]);
-        }
+          __stcs(Lb + c * LD + sidx, sidx == W ? 0.0 : P[(c + 1 + sidx) * LDP + c]);
+        const int ufirst = NBF - c;      // first U entry right of the block
+        for (int sidx = ufirst + lane; sidx < LD; sidx += 32)
+          __stcs(Ub + c * LD + sidx, U[c * LDU + c + sidx - NBF]);
       }
       __syncthreads();
       PHASE_MARK(6);

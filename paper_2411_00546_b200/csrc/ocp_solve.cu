@@ -10,8 +10,9 @@
 //   * the active part of the vector (W + 2 NB entries) lives in a circular
 //     shared buffer; finished forward values go to the output vector and
 //     come back for the backward sweep;
-//   * the in-block triangles were inverted at factorisation time, so each
-//     block costs two barrier-separated phases of independent FMAs:
+//   * blocks of 32 unknowns; the 32x32 diagonal triangles were inverted at
+//     factorisation time, so each block costs two barrier-separated phases of
+//     independent FMAs:
 //       forward  y_K = L11^{-1} b_K ;  b_{K+1..} -= L21 y_K
 //       backward x_K = U11^{-1} (z_K - U12 x_{K+1..})
 //
@@ -60,10 +61,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// circular vector window: >= W + 2 NB entries, power of two (index by mask)
+// circular vector window: >= W + 2 NBF entries, power of two (index by mask)
 __host__ __device__ __forceinline__ int ring_size(int w) {
   int r = 64;
-  while (r < w + 2 * NB) r <<= 1;
+  while (r < w + 2 * NBF) r <<= 1;
   return r;
 }
 
@@ -72,22 +73,23 @@ __global__ void __launch_bounds__(256, 2)
 k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
              double scale, double* out_pool, int max_w) {
   extern __shared__ __align__(16) double smem[];
-  const int SB = NB * (max_w + 1);                  // doubles per stage
+  constexpr int B = NBF;                            // 32 unknowns per factor block
+  const int SB = B * (max_w + 1);                   // doubles per stage
   const int RMAX = ring_size(max_w);
   double* stage = smem;                             // SOLVE_STAGES x SB
   double* ring = smem + SOLVE_STAGES * SB;          // RMAX (power of two)
-  double* ys = ring + RMAX;                         // NB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ys + NB);  // 2 x SOLVE_STAGES
+  double* ys = ring + RMAX;                         // B
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ys + B);  // 2 x SOLVE_STAGES
 
   const SubInfo s = subs[list[blockIdx.x]];
   const int tid = threadIdx.x;
-  const int W = s.W, LD = W + 1, NP = s.NP, nblk = NP / NB;
+  const int W = s.W, LD = W + 1, NP = s.NP, nblk = NP / B;
   const int RM = ring_size(W) - 1;                  // ring index mask
-  const long long bstride = 2LL * NB * LD;
+  const long long bstride = 2LL * B * LD;
   const double* fac = fac_pool + s.fac;
   double* zx = out_pool + s.loc;                    // z after the forward sweep, x after the backward
   const double* in = in_pool + s.loc;
-  const int gi = tid >> 4, gj = tid & 15;           // 16 x 16 thread grid for the block mat-vecs
+  const int gi = tid >> 3, gj = tid & 7;            // 32 x 8 thread grid for the block mat-vecs
 
   if (tid == 0) {
     for (int st = 0; st < 2 * SOLVE_STAGES; ++st) mbar_init(&bars[st], 1);
@@ -96,54 +98,58 @@ k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const
   for (int k = tid; k <= RM; k += blockDim.x) ring[k] = 0.0;
   __syncthreads();
   // ---------------- forward: L y = b ----------------
-  const uint32_t lbytes = (uint32_t)(NB * LD * sizeof(double));
+  const uint32_t lbytes = (uint32_t)(B * LD * sizeof(double));
   if (tid == 0) {
     for (int st = 0; st < SOLVE_STAGES && st < nblk; ++st) {
       mbar_expect_tx(&bars[st], lbytes);
       bulk_g2s(stage + st * SB, fac + st * bstride, lbytes, &bars[st]);
     }
   }
-  for (int k = tid; k < W + NB && k < NP; k += blockDim.x) ring[k & RM] = scale * in[k];
-  // rows entering the window at step K are [k0+NB+W, k0+2NB+W): prefetched one step ahead
+  for (int k = tid; k < W + B && k < NP; k += blockDim.x) ring[k & RM] = scale * in[k];
+  // rows entering the window at step K are [k0+B+W, k0+2B+W): prefetched one step ahead
   double rreg = 0.0;
-  if (tid < NB && NB + W + tid < NP) rreg = in[NB + W + tid];
+  if (tid < B && B + W + tid < NP) rreg = in[B + W + tid];
   __syncthreads();
   for (int K = 0; K < nblk; ++K) {
-    const int k0 = K * NB, st = K % SOLVE_STAGES;
+    const int k0 = K * B, st = K % SOLVE_STAGES;
     const double* Lb = stage + st * SB;
     mbar_wait(&bars[st], (K / SOLVE_STAGES) & 1);
-    {  // y_K = L11^{-1} b_K   (row gi, 16 lanes reduce over gj)
-      const double bj = ring[(k0 + gj) & RM];
-      const double l = Lb[gj * LD + ((gi - gj - 1) & 15)];
-      double v = gj < gi ? l * bj : (gj == gi ? bj : 0.0);
+    {  // y_K = L11^{-1} b_K   (row gi, 8 lanes reduce over j = gj + 8m)
+      double v = 0.0;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      for (int m = 0; m < 4; ++m) {
+        const int j = gj + 8 * m;
+        const double bj = ring[(k0 + j) & RM];
+        const double l = Lb[j * LD + ((gi - j - 1) & 31)];
+        v += j < gi ? l * bj : (j == gi ? bj : 0.0);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (gj == 0) ys[gi] = v;
     }
     __syncthreads();
-    if (tid < NB) {
+    if (tid < B) {
       const double y = ys[tid];
       ring[(k0 + tid) & RM] = y;
       zx[k0 + tid] = y;
-      const int r = k0 + NB + W + tid;               // entering row (slot of k0 - NB + tid)
+      const int r = k0 + B + W + tid;                // entering row (slot of k0 - B + tid)
       if (r < NP) ring[r & RM] = scale * rreg;
-      const int rn = r + NB;
+      const int rn = r + B;
       rreg = rn < NP ? in[rn] : 0.0;
     }
-    {  // b_r -= L21 y_K, r = k0 + NB + t
+    {  // b_r -= L21 y_K, r = k0 + B + t
       const int t = tid;
-      const int r = k0 + NB + t;
+      const int r = k0 + B + t;
       if (t < W && r < NP) {
-        const double* lp = Lb + (NB - 1) + t;        // column c entry at lp + c * (LD - 1)
-        // four independent accumulators: the 16-term dot is latency-bound otherwise
+        const double* lp = Lb + (B - 1) + t;         // column c entry at lp + c * (LD - 1)
         double acc[4] = {ring[r & RM], 0.0, 0.0, 0.0};
-        if (t + NB <= W) {
+        if (t + B <= W) {
 #pragma unroll
-          for (int c = 0; c < NB; ++c) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
+          for (int c = 0; c < B; ++c) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
         } else {
 #pragma unroll
-          for (int c = 0; c < NB; ++c)
-            if (NB - 1 + t - c < W) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
+          for (int c = 0; c < B; ++c)
+            if (B - 1 + t - c < W) acc[c & 3] = fma(-lp[c * (LD - 1)], ys[c], acc[c & 3]);
         }
         ring[r & RM] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
@@ -160,65 +166,70 @@ k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const
     const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
     kstop = 2 * s.nc * a_own;
   }
-  const uint32_t ubytes = (uint32_t)(NB * LD * sizeof(double));
+  const uint32_t ubytes = (uint32_t)(B * LD * sizeof(double));
   uint64_t* ubars = bars + SOLVE_STAGES;
   if (tid == 0) {
     for (int st = 0; st < SOLVE_STAGES && st < nblk; ++st) {
       const int K = nblk - 1 - st;
       mbar_expect_tx(&ubars[st], ubytes);
-      bulk_g2s(stage + st * SB, fac + K * bstride + NB * LD, ubytes, &ubars[st]);
+      bulk_g2s(stage + st * SB, fac + K * bstride + B * LD, ubytes, &ubars[st]);
     }
   }
   // ring slots of indices >= NP must read as 0 (their U entries are 0 too)
-  for (int k = NP + tid; k < NP + W + NB; k += blockDim.x) ring[k & RM] = 0.0;
+  for (int k = NP + tid; k < NP + W + B; k += blockDim.x) ring[k & RM] = 0.0;
   __syncthreads();
   // z of block K is in the ring when step K starts; z of K-1 is held in a
   // register one step ahead
-  if (tid < NB) ring[(NP - NB + tid) & RM] = zx[NP - NB + tid];
-  double zreg = (tid < NB && nblk >= 2) ? zx[NP - 2 * NB + tid] : 0.0;
-  const int MW = W / 16 + 1;  // band columns per lane (stride 16)
+  if (tid < B) ring[(NP - B + tid) & RM] = zx[NP - B + tid];
+  double zreg = (tid < B && nblk >= 2) ? zx[NP - 2 * B + tid] : 0.0;
+  const int MW = (W + 7) / 8 + 1;  // band columns per lane (stride 8)
   __syncthreads();
   int step = 0;
   for (; step < nblk; ++step) {
-    const int K = nblk - 1 - step, k0 = K * NB, st = step % SOLVE_STAGES;
-    if (k0 + NB <= kstop) break;
+    const int K = nblk - 1 - step, k0 = K * B, st = step % SOLVE_STAGES;
+    if (k0 + B <= kstop) break;
     const double* Ub = stage + st * SB;
     mbar_wait(&ubars[st], (step / SOLVE_STAGES) & 1);
-    {  // r_c = z_c - U12 x   (row gi, lanes gj stride 16 over the band)
+    {  // r_c = z_c - U12 x   (row gi, lanes gj stride 8 over the band)
       double acc0 = 0.0, acc1 = 0.0;
       const double* up = Ub + gi * LD;
       const int base = k0 + gi;
 #pragma unroll 4
       for (int m = 0; m < MW; m += 2) {
-        const int sidx = NB - gi + gj + 16 * m;
+        const int sidx = B - gi + gj + 8 * m;
         if (sidx <= W) acc0 = fma(up[sidx], ring[(base + sidx) & RM], acc0);
-        if (sidx + 16 <= W) acc1 = fma(up[sidx + 16], ring[(base + sidx + 16) & RM], acc1);
+        if (sidx + 8 <= W) acc1 = fma(up[sidx + 8], ring[(base + sidx + 8) & RM], acc1);
       }
       double acc = acc0 + acc1;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (gj == 0) ys[gi] = ring[(k0 + gi) & RM] - acc;
     }
     __syncthreads();
     {  // x_K = U11^{-1} r
-      const double u = Ub[gi * LD + ((gj - gi) & 15)];
-      double v = gj >= gi ? u * ys[gj] : 0.0;
+      double v = 0.0;
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      for (int m = 0; m < 4; ++m) {
+        const int j = gj + 8 * m;
+        const double u = Ub[gi * LD + ((j - gi) & 31)];
+        v += j >= gi ? u * ys[j] : 0.0;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (gj == 0) {
         ring[(k0 + gi) & RM] = v;
         zx[k0 + gi] = v;
       }
     }
-    if (tid < NB && k0 >= NB) {
-      ring[(k0 - NB + tid) & RM] = zreg;
-      zreg = k0 >= 2 * NB ? zx[k0 - 2 * NB + tid] : 0.0;
+    if (tid < B && k0 >= B) {
+      ring[(k0 - B + tid) & RM] = zreg;
+      zreg = k0 >= 2 * B ? zx[k0 - 2 * B + tid] : 0.0;
     }
     __syncthreads();
     if (tid == 0 && step + SOLVE_STAGES < nblk) {
       const int Kn = nblk - 1 - (step + SOLVE_STAGES);
       mbar_expect_tx(&ubars[st], ubytes);
-      bulk_g2s(stage + st * SB, fac + Kn * bstride + NB * LD, ubytes, &ubars[st]);
+      bulk_g2s(stage + st * SB, fac + Kn * bstride + B * LD, ubytes, &ubars[st]);
     }
   }
   // an early stop leaves up to SOLVE_STAGES bulk copies in flight: wait for
@@ -228,7 +239,7 @@ k_band_solve(const SubInfo* subs, const int* list, const double* fac_pool, const
 }
 
 size_t solve_smem_bytes(int max_w) {
-  return sizeof(double) * ((size_t)SOLVE_STAGES * NB * (max_w + 1) + ring_size(max_w) + NB) +
+  return sizeof(double) * ((size_t)SOLVE_STAGES * NBF * (max_w + 1) + ring_size(max_w) + NBF) +
          sizeof(uint64_t) * 2 * SOLVE_STAGES;
 }
 
