@@ -108,28 +108,32 @@ __device__ __forceinline__ double fast_rcp(double x) {
 
 // One warp factors the 16x16 block at P[(o+i)*LDP + o+j] in place (no
 // pivoting; L strict lower, U upper) and stores 1/U[i][i] in rd[i].
-// Shared-memory right-looking form: lane r < 16 owns row r, the pivot row is
-// read as a broadcast; no shuffles (their diverged-warp slow path cost 17x
-// inside this kernel).
-__device__ __forceinline__ void warp_lu16(double* P, int o, int lane, double* rd, int* bad) {
+// Compact on purpose: the step loop is not unrolled (the kernel's hot loop
+// must stay small for the instruction cache); lane r < 16 owns row r, loads
+// the pivot row and its own row into registers, updates, stores.
+__device__ __noinline__ void warp_lu16(double* P, int o, int lane, double* rd, int* bad) {
   __syncwarp();
   const int r = lane & 15;
   double* prow = P + (o + r) * LDP + o;
 #pragma unroll 1
   for (int c = 0; c < 16; ++c) {
     const double* pc = P + (o + c) * LDP + o;
+    double pv[16], a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) { pv[j] = pc[j]; a[j] = prow[j]; }
     const double piv = pc[c];
     const double rp = fast_rcp(piv);
     if (lane == 0) {
       rd[c] = rp;
       if (!(piv != 0.0 && isfinite(piv))) *bad = 1;
     }
+    __syncwarp();
     if (lane < 16 && r > c) {
       const double l = prow[c] * rp;
-      prow[c] = l;
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j > c) prow[j] = fma(-l, pc[j], prow[j]);
+      for (int j = 0; j < 16; ++j) a[j] = j > c ? fma(-l, pv[j], a[j]) : (j == c ? l : a[j]);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) prow[j] = a[j];
     }
     __syncwarp();
   }
@@ -217,41 +221,51 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       //         An entry (i, j) has been touched by an earlier panel update iff
       //         K > 0 and max(i, j) < k0 + W; all others still hold their
       //         original value and are generated here instead of stored.
+      //         Loads are issued in batches before any use (latency overlap).
       {
         const int fresh = K == 0 ? k0 : k0 + W;   // indices >= fresh are untouched
         int pcol = ks + lane; pcol -= pcol >= WS ? WS : 0;
-        for (int r = warp; r < W + NBF; r += NW) {
-          const int i = k0 + r;
-          double v;
-          if (i >= fresh || k0 + lane >= fresh) {
-            v = entry(s, row_info(s, JD, i), k0 + lane, off);
-          } else {
+        constexpr int PB = 8;
+        for (int r0 = warp; r0 < W + NBF; r0 += PB * NW) {
+          double v[PB];
+#pragma unroll
+          for (int q = 0; q < PB; ++q) {
+            const int r = r0 + q * NW;
             int pr = ks + r; pr -= pr >= WS ? WS : 0; pr -= pr >= WS ? WS : 0;
-            v = win[(long long)pr * WS + pcol];
+            v[q] = (r < W + NBF && k0 + r < fresh && k0 + lane < fresh)
+                       ? win[(long long)pr * WS + pcol] : 0.0;
           }
-          P[r * LDP + lane] = v;
+#pragma unroll
+          for (int q = 0; q < PB; ++q) {
+            const int r = r0 + q * NW, i = k0 + r;
+            if (r < W + NBF) {
+              if (i >= fresh || k0 + lane >= fresh) v[q] = entry(s, row_info(s, JD, i), k0 + lane, off);
+              P[r * LDP + lane] = v[q];
+            }
+          }
         }
         for (int t = warp; t < NBF; t += NW) {
           const int i = k0 + t;
           int pr = ks + t; pr -= pr >= WS ? WS : 0;
           const double* src = win + (long long)pr * WS;
-          const RowInfo ri = row_info(s, JD, i);
           double v[8];
           int pc = ks + NBF + lane; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int c = lane + 32 * q, j = k0 + NBF + c;
-            v[q] = c >= W ? 0.0 : (j >= fresh || i >= fresh) ? entry(s, ri, j, off) : src[pc];
+            v[q] = (c < W && j < fresh && i < fresh) ? src[pc] : 0.0;
             pc += 32;
             pc -= pc >= WS ? WS : 0;
           }
+          const RowInfo ri = row_info(s, JD, i);
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (lane + 32 * q < W) U[t * LDU + lane + 32 * q] = v[q];
+          for (int q = 0; q < 8; ++q) {
+            const int c = lane + 32 * q, j = k0 + NBF + c;
+            if (c < W) U[t * LDU + c] = (j >= fresh || i >= fresh) ? entry(s, ri, j, off) : v[q];
+          }
         }
       }
       __syncthreads();
-      PHASE_MARK(1);
       // ---- 2a. LU(A_aa) (warp 0)
       if (warp == 0) warp_lu16(P, 0, lane, rd[0], &bad);
       __syncthreads();
@@ -385,44 +399,46 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
           for (int i = 0; i < 16; ++i) __stcs(Ub + i * LD + (16 + j) - i, t[i]);   // Y[i][j]
         }
       }
-      // ---- 3b. rank-32 trailing update on [k0+32, k0+32+W)^2 with DMMA
+      // ---- 3b. rank-32 trailing update on [k0+32, k0+32+W)^2 with DMMA,
+      //          32x16 warp tiles (4x2 m8n8k4 tiles, 8 independent accumulators)
       {
-        const int TW = W >> 4, g = lane >> 2, t4 = lane & 3;
-        for (int wt = (warp + 1) & (NW - 1); wt < TW * TW; wt += NW) {
-          const int tr = wt / TW, tc = wt - tr * TW;
-          const int R0 = 16 * tr, C0 = 16 * tc;
-          double c[2][2][2];
-          long long addr[2][2];
-          // the last 32 rows/columns of the window (and all of it in panel 0)
-          // have never been updated: generated, not loaded
-          const bool gen = K == 0 || R0 + 16 > W - NBF || C0 + 16 > W - NBF;
+        const int g = lane >> 2, t4 = lane & 3;
+        const int TR = (W + 31) >> 5, TC = W >> 4;     // last tile row may be 16 rows
+        const int fresh = K == 0 ? k0 : k0 + W;        // indices >= fresh never updated
+        for (int wt = (warp + 1) & (NW - 1); wt < TR * TC; wt += NW) {
+          const int tr = wt / TC, tc = wt - tr * TC;
+          const int R0 = 32 * tr, C0 = 16 * tc;
+          const int mrows = (W - R0) >= 32 ? 4 : 2;    // 8-row slabs in this tile
+          double c[4][2][2];
+          long long addr[4][2];
+          const bool gen = K == 0 || R0 + 32 > W - NBF || C0 + 16 > W - NBF;
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
+          for (int mi = 0; mi < 4; ++mi) {
             int pr = ks + NBF + R0 + 8 * mi + g; pr -= pr >= WS ? WS : 0; pr -= pr >= WS ? WS : 0;
 #pragma unroll
             for (int ni = 0; ni < 2; ++ni) {
               int pc = ks + NBF + C0 + 8 * ni + 2 * t4; pc -= pc >= WS ? WS : 0; pc -= pc >= WS ? WS : 0;
               addr[mi][ni] = (long long)pr * WS + pc;
-              if (!gen) {
+              c[mi][ni][0] = c[mi][ni][1] = 0.0;
+              if (mi < mrows) {
                 const double2 v = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
                 c[mi][ni][0] = v.x;
                 c[mi][ni][1] = v.y;
-              } else {
-                const int i = k0 + NBF + R0 + 8 * mi + g, j = k0 + NBF + C0 + 8 * ni + 2 * t4;
-                const int fresh = K == 0 ? k0 : k0 + W;
-                double v0, v1;
-                if (i >= fresh || j + 1 >= fresh) {
-                  const RowInfo ri = row_info(s, JD, i);
-                  const double2 w = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
-                  v0 = (i >= fresh || j >= fresh) ? entry(s, ri, j, off) : w.x;
-                  v1 = entry(s, ri, j + 1, off);
-                } else {
-                  const double2 w = *reinterpret_cast<const double2*>(win + addr[mi][ni]);
-                  v0 = w.x;
-                  v1 = w.y;
+              }
+            }
+          }
+          if (gen) {   // overwrite the entries that are still original with generated values
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+              const int i = k0 + NBF + R0 + 8 * mi + g;
+              if (mi < mrows) {
+                const RowInfo ri = row_info(s, JD, i);
+#pragma unroll
+                for (int ni = 0; ni < 2; ++ni) {
+                  const int j = k0 + NBF + C0 + 8 * ni + 2 * t4;
+                  if (i >= fresh || j >= fresh) c[mi][ni][0] = entry(s, ri, j, off);
+                  if (i >= fresh || j + 1 >= fresh) c[mi][ni][1] = entry(s, ri, j + 1, off);
                 }
-                c[mi][ni][0] = v0;
-                c[mi][ni][1] = v1;
               }
             }
           }
@@ -430,18 +446,22 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
           const double* bp = U + t4 * LDU + C0 + g;
 #pragma unroll
           for (int kk = 0; kk < NBF; kk += 4) {
-            const double a0 = -ap[kk], a1 = -ap[8 * LDP + kk];
             const double b0 = bp[kk * LDU], b1 = bp[kk * LDU + 8];
-            dmma_884(c[0][0][0], c[0][0][1], a0, b0);
-            dmma_884(c[0][1][0], c[0][1][1], a0, b1);
-            dmma_884(c[1][0][0], c[1][0][1], a1, b0);
-            dmma_884(c[1][1][0], c[1][1][1], a1, b1);
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {
+              if (mi < mrows) {
+                const double am = -ap[8 * mi * LDP + kk];
+                dmma_884(c[mi][0][0], c[mi][0][1], am, b0);
+                dmma_884(c[mi][1][0], c[mi][1][1], am, b1);
+              }
+            }
           }
 #pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
+          for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
             for (int ni = 0; ni < 2; ++ni)
-              *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
+              if (mi < mrows)
+                *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
         }
       }
       // ---- 3c. the rest of the finished 32-block -> factor store
