@@ -263,7 +263,15 @@ def run_ours(args):
     sol_bytes = st["solve_bytes"] / max(st["solve_launches"], 1)
     fac_tf = fac_flops / (fac_avg_ms * 1e-3) / 1e12 if fac_avg_ms > 0 else None
     sol_gbs = sol_bytes / (sol_avg_ms * 1e-3) / 1e9 if sol_avg_ms > 0 else None
+    res_avg_ms = st["resid_ms"] / max(st["resid_launches"], 1)
+    res_bytes = st["resid_bytes"] / max(st["resid_launches"], 1)
+    res_gbs = res_bytes / (res_avg_ms * 1e-3) / 1e9 if res_avg_ms > 0 else None
     kernels = {
+        "local_residual_stencil": {"bound": "hbm", "achieved": res_gbs, "peak": hbm, "unit": "GB/s",
+                                   "frac": (res_gbs / hbm) if res_gbs and hbm else None,
+                                   "launches": st["resid_launches"], "avg_ms": res_avg_ms,
+                                   "share_of_step": st["resid_ms"] / ms_total,
+                                   "algorithmic_bytes_per_launch": res_bytes},
         "band_factor": {"bound": "fp64", "achieved": fac_tf, "peak": fp64_tf, "unit": "TFLOP/s",
                         "frac": (fac_tf / fp64_tf) if fac_tf and fp64_tf else None,
                         "peak_source": fp64_src, "launches": st["factor_launches"],
@@ -276,7 +284,7 @@ def run_ours(args):
                            "share_of_step": st["solve_ms"] / ms_total,
                            "algorithmic_bytes_per_launch": sol_bytes},
     }
-    dominant = max(kernels, key=lambda k: kernels[k]["share_of_step"])
+    dominant = max(kernels, key=lambda k: kernels[k]["share_of_step"] or 0.0)
     kd = kernels[dominant]
     roofline = {"kernel": dominant, "bound": kd["bound"], "achieved": kd["achieved"],
                 "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"], "traffic": None}

@@ -144,7 +144,8 @@ int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps,
  * stats[0]=kernel launches, [1]=factor ms, [2]=factor launches,
  * [3]=solve ms (stored-factor JVP solves), [4]=solve launches,
  * [5]=factor flops, [6]=JVP-solve factor bytes, [7]=residual-sweep ms,
- * [8]=DOF-updates, [9]=jvp ms, [10]=inner-solve ms, [11]=mgs ms
+ * [8]=DOF-updates, [9]=jvp ms, [10]=inner-solve ms, [11]=mgs ms,
+ * [12]=full-set local-residual ms, [13]=its launches, [14]=its algorithmic bytes
  * Times need ocp_set_profiling(ctx, 1) (CUDA events on the context stream). */
 int ocp_set_profiling(ocp_ctx* ctx, int on);
 int ocp_stats(ocp_ctx* ctx, double* stats, int len);

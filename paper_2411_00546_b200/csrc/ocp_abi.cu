@@ -33,7 +33,8 @@ struct Event {
   double flops, bytes;
 };
 
-enum { CLS_FACTOR = 0, CLS_SOLVE = 1, CLS_SWEEP = 2, CLS_JVP = 3, CLS_INNER_SOLVE = 4, CLS_MGS = 5 };
+enum { CLS_FACTOR = 0, CLS_SOLVE = 1, CLS_SWEEP = 2, CLS_JVP = 3, CLS_INNER_SOLVE = 4, CLS_MGS = 5,
+       CLS_RESID = 6, NCLS = 7 };
 
 }  // namespace
 
@@ -52,7 +53,9 @@ struct ocp_ctx {
   double *d_f = nullptr, *d_yd = nullptr;
   double *V = nullptr, *R = nullptr, *D = nullptr, *B = nullptr, *JD = nullptr;
   int *d_list_all = nullptr, *d_list = nullptr, *d_status = nullptr, *d_flags = nullptr;
-  double *d_alpha = nullptr, *d_norm2 = nullptr;
+  double *d_alpha = nullptr, *d_norm2 = nullptr, *d_rpart = nullptr;
+  unsigned int* d_rcount = nullptr;
+  int res_chunks = 1;
   long long* d_bad = nullptr;
   double* scratch = nullptr;
   long long ws_stride = 0;
@@ -75,9 +78,10 @@ struct ocp_ctx {
   long long launches = 0;
   std::vector<Event> pending;
   std::vector<cudaEvent_t> free_events;
-  double stat_ms[6] = {0, 0, 0, 0, 0, 0};
-  double stat_cnt[6] = {0, 0, 0, 0, 0, 0};
-  double stat_flops = 0, stat_bytes = 0, stat_dof = 0;
+  double stat_ms[NCLS] = {};
+  double stat_cnt[NCLS] = {};
+  double stat_flops = 0, stat_bytes = 0, stat_dof = 0, stat_rbytes = 0;
+  double resid_bytes_all = 0;   // algorithmic bytes of one full-set residual
   cudaEvent_t marks[16] = {};
 };
 
@@ -125,7 +129,7 @@ struct Timer {
   ocp_ctx* ctx;
   Event ev{};
   bool on;
-  Timer(ocp_ctx* c, int cls, double flops = 0, double bytes = 0) : ctx(c), on(c->prof) {
+  Timer(ocp_ctx* c, int cls, double flops = 0, double bytes = 0) : ctx(c), on(c && c->prof) {
     if (!on) return;
     ev.a = get_event(ctx);
     ev.b = get_event(ctx);
@@ -151,6 +155,7 @@ void drain_events(ocp_ctx* ctx) {
     ctx->stat_cnt[e.cls] += 1;
     if (e.cls == CLS_FACTOR) ctx->stat_flops += e.flops;
     if (e.cls == CLS_SOLVE) ctx->stat_bytes += e.bytes;
+    if (e.cls == CLS_RESID) ctx->stat_rbytes += e.bytes;
     ctx->free_events.push_back(e.a);
     ctx->free_events.push_back(e.b);
   }
@@ -176,6 +181,21 @@ double band_lu_flops(long long N, long long w) {
   return tot;
 }
 
+
+// local residual (+ per-subdomain squared norms) of `cnt` listed subdomains
+int launch_residual(ocp_ctx* ctx, const int* d_list, int cnt, const double* x, const double* V,
+                    const double* D, const double* alpha, double eps, double* R) {
+  if (cnt == 0) return OCP_OK;
+  // full-set residual evaluations are timed for the stencil roofline
+  // (48 B per local point: read y,p,f,y_d, write r1,r2 - SURVEY.md 8d)
+  Timer t(cnt == ctx->I && !D ? ctx : nullptr, CLS_RESID, 0, ctx->resid_bytes_all);
+  const dim3 grid(cnt, ctx->res_chunks);
+  k_residual<<<grid, 256, 0, ctx->stream>>>(ctx->d_subs, d_list, ctx->P, x, V, D, alpha, ctx->d_f,
+                                             ctx->d_yd, eps, R, ctx->d_norm2, ctx->d_rpart,
+                                             ctx->d_rcount);
+  CKL();
+  return OCP_OK;
+}
 
 int upload_list(ocp_ctx* ctx, const std::vector<int>& list) {
   std::copy(list.begin(), list.end(), ctx->h_list);
@@ -357,6 +377,15 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(cudaMalloc(&ctx->d_status, I * sizeof(int)));
   CKC(cudaMalloc(&ctx->d_alpha, I * sizeof(double)));
   CKC(cudaMalloc(&ctx->d_norm2, I * sizeof(double)));
+  {
+    // residual grid: one CTA per 32x32 tile of the oriented local grid
+    int maxt = 1;
+    for (auto& sub : ctx->subs) maxt = std::max(maxt, ((sub.nr + 31) / 32) * ((sub.nc + 31) / 32));
+    ctx->res_chunks = maxt;
+  }
+  CKC(cudaMalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
+  CKC(cudaMalloc(&ctx->d_rcount, I * sizeof(unsigned int)));
+  CKC(cudaMemset(ctx->d_rcount, 0, I * sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->d_bad, I * sizeof(long long)));
   CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(int)));
   {
@@ -404,7 +433,10 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     CKC(set_band_solve_smem(solve_smem));
   }
 #undef CKC
-  for (auto& s : ctx->subs) ctx->dof_total += s.N;
+  for (auto& s : ctx->subs) {
+    ctx->dof_total += s.N;
+    ctx->resid_bytes_all += 48.0 * (double)s.nr * s.nc;
+  }
   *out = ctx;
   return OCP_OK;
 }
@@ -415,7 +447,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_flags, (void*)ctx->scratch,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
@@ -522,9 +554,7 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
   k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->V);
   CKL();
   double eps = eps0;
-  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->V, nullptr, nullptr,
-                                ctx->d_f, ctx->d_yd, eps, ctx->R, ctx->d_norm2);
-  CKL();
+  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->V, nullptr, nullptr, eps, ctx->R)) return rc;
   CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int i = 0; i < I; ++i) {
@@ -584,10 +614,8 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
       for (size_t k = 0; k < pend.size(); ++k) ctx->h_alpha[pend[k]] = alpha[pend[k]];
       CK(cudaMemcpyAsync(ctx->d_alpha, ctx->h_alpha, I * sizeof(double), cudaMemcpyHostToDevice, st));
       if (int rc = upload_list(ctx, pend)) return rc;
-      k_residual<<<(int)pend.size(), 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, x, ctx->V,
-                                                    ctx->D, ctx->d_alpha, ctx->d_f, ctx->d_yd, eps,
-                                                    nullptr, ctx->d_norm2);
-      CKL();
+      if (int rc = launch_residual(ctx, ctx->d_list, (int)pend.size(), x, ctx->V, ctx->D,
+                                   ctx->d_alpha, eps, nullptr)) return rc;
       CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       next.clear();
@@ -616,9 +644,8 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
       const int na = (int)acc.size();
       k_update<<<na, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->V, ctx->D, ctx->d_alpha);
       CKL();
-      k_residual<<<na, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, x, ctx->V, nullptr, nullptr,
-                                     ctx->d_f, ctx->d_yd, eps_next, ctx->R, ctx->d_norm2);
-      CKL();
+      if (int rc = launch_residual(ctx, ctx->d_list, na, x, ctx->V, nullptr, nullptr, eps_next, ctx->R))
+        return rc;
       CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       for (int i : acc) {
@@ -698,9 +725,7 @@ int ocp_local_residual(ocp_ctx* ctx, const double* x, const double* v_ref, doubl
   const int I = ctx->I;
   k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
   CKL();
-  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->B, nullptr, nullptr,
-                                ctx->d_f, ctx->d_yd, eps, ctx->D, ctx->d_norm2);
-  CKL();
+  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->B, nullptr, nullptr, eps, ctx->D)) return rc;
   k_band_to_ref<<<I, 256, 0, st>>>(ctx->d_subs, ctx->D, r_ref);
   CKL();
   CK(cudaStreamSynchronize(st));
@@ -714,9 +739,7 @@ int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, doub
   CK(cudaMalloc(&fac, ctx->fac_len * sizeof(double)));
   k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
   CKL();
-  k_residual<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->B, nullptr, nullptr,
-                                ctx->d_f, ctx->d_yd, eps, ctx->D, ctx->d_norm2);
-  CKL();
+  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->B, nullptr, nullptr, eps, ctx->D)) return rc;
   k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->B, eps, ctx->JD, ctx->d_bad);
   CKL();
   std::vector<int> all(I);
@@ -900,11 +923,12 @@ int ocp_set_profiling(ocp_ctx* ctx, int on) {
 int ocp_stats(ocp_ctx* ctx, double* stats, int len) {
   if (!ctx || !stats) return OCP_ERR_ARG;
   drain_events(ctx);
-  double v[12] = {(double)ctx->launches, ctx->stat_ms[CLS_FACTOR], ctx->stat_cnt[CLS_FACTOR],
+  double v[15] = {(double)ctx->launches, ctx->stat_ms[CLS_FACTOR], ctx->stat_cnt[CLS_FACTOR],
                   ctx->stat_ms[CLS_SOLVE], ctx->stat_cnt[CLS_SOLVE], ctx->stat_flops,
                   ctx->stat_bytes, ctx->stat_ms[CLS_SWEEP], ctx->stat_dof, ctx->stat_ms[CLS_JVP],
-                  ctx->stat_ms[CLS_INNER_SOLVE], ctx->stat_ms[CLS_MGS]};
-  for (int i = 0; i < len && i < 12; ++i) stats[i] = v[i];
+                  ctx->stat_ms[CLS_INNER_SOLVE], ctx->stat_ms[CLS_MGS], ctx->stat_ms[CLS_RESID],
+                  ctx->stat_cnt[CLS_RESID], ctx->stat_rbytes};
+  for (int i = 0; i < len && i < 15; ++i) stats[i] = v[i];
   return OCP_OK;
 }
 
@@ -912,8 +936,8 @@ int ocp_reset_stats(ocp_ctx* ctx) {
   if (!ctx) return OCP_ERR_ARG;
   drain_events(ctx);
   ctx->launches = 0;
-  for (int i = 0; i < 6; ++i) ctx->stat_ms[i] = ctx->stat_cnt[i] = 0;
-  ctx->stat_flops = ctx->stat_bytes = ctx->stat_dof = 0;
+  for (int i = 0; i < NCLS; ++i) ctx->stat_ms[i] = ctx->stat_cnt[i] = 0;
+  ctx->stat_flops = ctx->stat_bytes = ctx->stat_dof = ctx->stat_rbytes = 0;
   return OCP_OK;
 }
 

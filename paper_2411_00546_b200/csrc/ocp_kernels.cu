@@ -105,36 +105,160 @@ __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const dou
 // local residual (+ squared norm) of the listed subdomains at V + alpha_i D
 // _local_problem.local_residual (schwarz.py:181-186); R may be null (trial)
 // ---------------------------------------------------------------------------
+// Shared-memory halo tiles: a CTA owns a 32x32 tile of the oriented local
+// grid.  The (v + alpha d) tile plus its 1-point halo is staged in shared
+// memory with loads coalesced in local (band) order; the points are then
+// evaluated with threads running fast along the GLOBAL column index, so the
+// f / y_d / exterior-ring reads are coalesced for both orientations; the
+// residual tile goes back through shared memory to be stored in local order.
+constexpr int RT = 32;   // tile edge (oriented points)
+
 __global__ void __launch_bounds__(256) k_residual(const SubInfo* subs, const int* list, Phys P,
                                                   const double* x, const double* Vpool,
                                                   const double* Dpool, const double* alpha,
                                                   const double* f, const double* yd, double eps,
-                                                  double* Rpool, double* norm2) {
+                                                  double* Rpool, double* norm2, double* partials,
+                                                  unsigned int* counters) {
+  __shared__ double2 tv[(RT + 2) * (RT + 2)];   // halo tile of v + alpha d, [a+1][b+1];
+                                                // reused for the residual tile [a][b] (+1 pad)
+  double2* tr = tv;
   __shared__ double red[32];
+  __shared__ bool is_last;
   const int sid = list[blockIdx.x];
   const SubInfo s = subs[sid];
   const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
   const double2* D = Dpool ? reinterpret_cast<const double2*>(Dpool + s.loc) : nullptr;
   double2* R = Rpool ? reinterpret_cast<double2*>(Rpool + s.loc) : nullptr;
-  const double a = alpha ? alpha[sid] : 0.0;
+  const double al = alpha ? alpha[sid] : 0.0;
   const long long Ntot = (long long)P.n * P.n;
-  const int real = s.nr * s.nc;
+  const int tb_n = (s.nc + RT - 1) / RT;
+  const int tile = blockIdx.y;
+  const int a0 = (tile / tb_n) * RT, b0 = (tile % tb_n) * RT;
   double acc = 0.0;
-  for (int q = threadIdx.x; q < real; q += blockDim.x) {
-    int i, j;
-    local_to_global(s, q / s.nc, q % s.nc, i, j);
-    double ay, ap;
-    stencil_point(s, P, V, D, a, x, Ntot, i, j, ay, ap);
-    const double2 v = lval(V, D, a, q);
-    const long long g = (long long)i * P.n + j;
-    double r1, r2;
-    residual_rows(P, ay, ap, v.x, v.y, f[g], yd[g], eps, r1, r2);
-    if (R) R[q] = make_double2(r1, r2);
-    acc = fma(r1, r1, acc);
-    acc = fma(r2, r2, acc);
+  if (a0 < s.nr) {
+    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
+    const int n = P.n;
+    // 0. issue this thread's f / y_d loads first (independent of the tile)
+    double fv[RT / 8], ydv[RT / 8];
+#pragma unroll
+    for (int u = 0; u < RT / 8; ++u) {
+      const int k = row + 8 * u;
+      const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
+      const int la = a0 + ta, lb = b0 + tbb;
+      fv[u] = ydv[u] = 0.0;
+      if (la < s.nr && lb < s.nc) {
+        int i, j;
+        local_to_global(s, la, lb, i, j);
+        const long long g = (long long)i * n + j;
+        fv[u] = f[g];
+        ydv[u] = yd[g];
+      }
+    }
+    // 1. stage the halo tile (local order, coalesced along b)
+    for (int e = threadIdx.x; e < (RT + 2) * (RT + 2); e += blockDim.x) {
+      const int ta = e / (RT + 2), tbb = e - ta * (RT + 2);
+      const int la = a0 + ta - 1, lb = b0 + tbb - 1;
+      double2 v = make_double2(0.0, 0.0);
+      if (la >= 0 && la < s.nr && lb >= 0 && lb < s.nc) v = lval(V, D, al, la * s.nc + lb);
+      tv[e] = v;
+    }
+    __syncthreads();
+    // 2. evaluate, threads fast along the global column
+    double2 res[RT / 8];
+#pragma unroll
+    for (int u = 0; u < RT / 8; ++u) {
+      res[u] = make_double2(0.0, 0.0);
+      const int k = row + 8 * u;
+      // orient 0: global column = b -> (a, b) = (k, lane); orient 1: column = a -> (lane, k)
+      const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
+      const int la = a0 + ta, lb = b0 + tbb;
+      if (la >= s.nr || lb >= s.nc) continue;
+      int i, j;
+      local_to_global(s, la, lb, i, j);
+      // neighbours in ascending global column order (csr_matvec), local part
+      // from the tile, exterior part from the frozen global iterate
+      double sly = 0.0, slp = 0.0, sey = 0.0, sep = 0.0;
+      const double2* c = tv + (ta + 1) * (RT + 2) + tbb + 1;
+      if (la > 0 && la < s.nr - 1 && lb > 0 && lb < s.nc - 1) {
+        // interior of the rectangle: all five entries are local; tile
+        // offsets of (i-1,j), (i,j-1), (i,j+1), (i+1,j) for this orientation
+        const int o1 = s.orient == 0 ? -(RT + 2) : -1;
+        const int o2 = s.orient == 0 ? -1 : -(RT + 2);
+        const double2 v1 = c[o1], v2 = c[o2], v3 = c[0], v4 = c[-o2], v5 = c[-o1];
+        sly = add(0.0, mul(P.off, v1.x));   // csr_matvec starts its sum at 0.0
+        slp = add(0.0, mul(P.off, v1.y));
+        sly = add(sly, mul(P.off, v2.x));
+        slp = add(slp, mul(P.off, v2.y));
+        sly = add(sly, mul(P.diag, v3.x));
+        slp = add(slp, mul(P.diag, v3.y));
+        sly = add(sly, mul(P.off, v4.x));
+        slp = add(slp, mul(P.off, v4.y));
+        sly = add(sly, mul(P.off, v5.x));
+        slp = add(slp, mul(P.off, v5.y));
+        sly = add(sly, 0.0);   // the empty exterior part (csr sum of no terms is 0.0)
+        slp = add(slp, 0.0);
+      } else {
+        const int di[5] = {-1, 0, 0, 0, 1};
+        const int dj[5] = {0, -1, 0, 1, 0};
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+          const int ii = i + di[t], jj = j + dj[t];
+          if (ii < 0 || ii >= n || jj < 0 || jj >= n) continue;
+          const double coef = (t == 2) ? P.diag : P.off;
+          if (in_rect(s, ii, jj)) {
+            // oriented offsets of the neighbour inside the tile (+1 halo)
+            const int na = s.orient == 0 ? ii - s.r0 : jj - s.c0;
+            const int nbb = s.orient == 0 ? jj - s.c0 : ii - s.r0;
+            const double2 v = tv[(na - a0 + 1) * (RT + 2) + (nbb - b0 + 1)];
+            sly = add(sly, mul(coef, v.x));
+            slp = add(slp, mul(coef, v.y));
+          } else {
+            const long long g = (long long)ii * n + jj;
+            sey = add(sey, mul(coef, x[g]));
+            sep = add(sep, mul(coef, x[Ntot + g]));
+          }
+        }
+      }
+      const double ay = add(sly, sey), ap = add(slp, sep);
+      const double2 v = c[0];
+      double r1, r2;
+      residual_rows(P, ay, ap, v.x, v.y, fv[u], ydv[u], eps, r1, r2);
+      res[u] = make_double2(r1, r2);
+      acc = fma(r1, r1, acc);
+      acc = fma(r2, r2, acc);
+    }
+    // 3. residual tile back in local order (through the staging tile)
+    if (R) {
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < RT / 8; ++u) {
+        const int k = row + 8 * u;
+        const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
+        tr[ta * (RT + 1) + tbb] = res[u];
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < RT * RT; e += blockDim.x) {
+        const int ta = e / RT, tbb = e - ta * RT;
+        const int la = a0 + ta, lb = b0 + tbb;
+        if (la < s.nr && lb < s.nc) R[la * s.nc + lb] = tr[ta * (RT + 1) + tbb];
+      }
+    }
   }
   const double tot = block_sum<256>(acc, red);
-  if (threadIdx.x == 0) norm2[sid] = tot;
+  if (threadIdx.x == 0) {
+    partials[(long long)sid * gridDim.y + blockIdx.y] = tot;
+    __threadfence();
+    const unsigned int ticket = atomicAdd(&counters[sid], 1u);
+    is_last = (ticket == gridDim.y - 1);
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double v = 0.0;
+    for (int y = 0; y < (int)gridDim.y; ++y) v += partials[(long long)sid * gridDim.y + y];
+    norm2[sid] = v;
+    counters[sid] = 0u;
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -90,11 +90,11 @@ class Engine:
         self.check(self.lib.ocp_set_profiling(self.ctx, 1 if on else 0), "ocp_set_profiling")
 
     def stats(self):
-        buf = (ctypes.c_double * 12)()
-        self.check(self.lib.ocp_stats(self.ctx, buf, 12), "ocp_stats")
+        buf = (ctypes.c_double * 15)()
+        self.check(self.lib.ocp_stats(self.ctx, buf, 15), "ocp_stats")
         keys = ("launches", "factor_ms", "factor_launches", "solve_ms", "solve_launches",
                 "factor_flops", "solve_bytes", "sweep_ms", "dof_updates", "jvp_ms",
-                "inner_solve_ms", "mgs_ms")
+                "inner_solve_ms", "mgs_ms", "resid_ms", "resid_launches", "resid_bytes")
         return dict(zip(keys, list(buf)))
 
     def mark(self, slot):

@@ -34,7 +34,8 @@ for r in range(reps):
     print("    stats", json.dumps({k: round(v, 3) for k, v in st.items()}))
     if st["factor_ms"] > 0:
         print(f"    factor {st['factor_flops']/st['factor_ms']/1e9:.2f} TFLOP/s over {st['factor_launches']:.0f} launches; "
-              f"jvp-solve {st['solve_bytes']/max(st['solve_ms'],1e-9)/1e6:.1f} GB/s over {st['solve_launches']:.0f}")
+              f"jvp-solve {st['solve_bytes']/max(st['solve_ms'],1e-9)/1e6:.1f} GB/s over {st['solve_launches']:.0f}; "
+              f"residual {st['resid_bytes']/max(st['resid_ms'],1e-9)/1e6:.1f} GB/s over {st['resid_launches']:.0f}")
 if x is not None and len(sys.argv) > 4:
     np.save(sys.argv[4], x.to_host())
 
