@@ -37,7 +37,8 @@ typedef enum {
   OCP_ERR_NONFINITE = 4,      /* NonfiniteFieldError(where, index), grid.py:9-23 */
   OCP_ERR_NONFINITE_INIT = 5, /* ValueError("nonfinite residual at the initial guess"), newton.py:146-147 */
   OCP_ERR_UNSUPPORTED = 6,    /* shape outside the compiled kernel limits */
-  OCP_ERR_NO_DEVICE = 7
+  OCP_ERR_NO_DEVICE = 7,
+  OCP_ERR_GMRES_BREAKDOWN = 8 /* GmresBreakdownError, krylov.py:15 */
 } ocp_status;
 
 /* phi selector: kappa*(s^3+e^{kappa s}) (system.py:31-74), y^3, e^y-1 */
@@ -133,6 +134,17 @@ int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j,
  * Single cooperative kernel; falls back to per-pass kernels for large n. */
 int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j,
                 const double* w_in, double* h_host);
+/* Unpreconditioned, unrestarted MGS-GMRES on the RASPEN Jacobian action
+ * (the configuration raspen_solve uses: newton.py:115-124 with precond None,
+ * krylov.py:44-151 with x0 None).  Everything of one GMRES solve in one
+ * call: JVPs and Arnoldi steps on the device, Givens rotations / back
+ * substitution on the host in float64 with the reference's operation order.
+ *   b_dev  [n] right-hand side;  x_dev [n] solution (written)
+ *   history_host [max_iters+1] residual history (len = iters + 1)
+ * Returns OCP_ERR_GMRES_BREAKDOWN for nonfinite Arnoldi entries. */
+int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac_dev, const double* b_dev, double rel_tol,
+                     double abs_tol, int max_iters, double* x_dev, int* iters_host,
+                     double* residual_host, int* converged_host, double* history_host);
 /* out = x + Q[:, :k] @ y  (krylov.py:151) */
 int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k,
                  const double* y_host, const double* x, double* out);

@@ -21,6 +21,7 @@ OCP_ERR_NONFINITE = 4
 OCP_ERR_NONFINITE_INIT = 5
 OCP_ERR_UNSUPPORTED = 6
 OCP_ERR_NO_DEVICE = 7
+OCP_ERR_GMRES_BREAKDOWN = 8
 
 _c_int_p = ctypes.POINTER(ctypes.c_int)
 _c_dbl_p = ctypes.POINTER(ctypes.c_double)
@@ -58,6 +59,7 @@ SIGNATURES = {
     "ocp_vec_all_finite": [_vp, _ll, _vp, _c_int_p],
     "ocp_mgs": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
     "ocp_arnoldi": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
+    "ocp_raspen_gmres": [_vp, _vp, _vp, _d, _d, _i, _vp, _c_int_p, _c_dbl_p, _c_int_p, _c_dbl_p],
     "ocp_gemv_add": [_vp, _ll, _vp, _ll, _i, _c_dbl_p, _vp, _vp],
     "ocp_recover_control": [_vp, _ll, _vp, _d, _vp],
     "ocp_set_profiling": [_vp, _i],

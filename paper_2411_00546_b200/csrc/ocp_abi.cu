@@ -62,6 +62,9 @@ struct ocp_ctx {
   int lu_grid = 1, num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
+  double* gm_Q = nullptr;      // persistent GMRES basis (grow-only), ocp_raspen_gmres
+  double* gm_w = nullptr;
+  long long gm_cols = 0;
   int h_cap = 0;
   cudaStream_t stream = nullptr;
   // pinned host staging
@@ -449,6 +452,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
                   (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
+                  (void*)ctx->gm_Q, (void*)ctx->gm_w,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
@@ -890,6 +894,122 @@ int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j, cons
   }
   CK(cudaMemcpyAsync(h_host, ctx->d_h, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return OCP_OK;
+}
+
+// GMRES for the RASPEN operator, the whole solve in native code
+// (krylov.py:44-151 with precond = None, x0 = None, restart = None).
+int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double rel_tol,
+                     double abs_tol, int max_iters, double* x, int* iters_out, double* resid_out,
+                     int* conv_out, double* history) {
+  if (!ctx || !fac || !b || !x || max_iters < 1) return fail(ctx, OCP_ERR_ARG, "bad argument");
+  cudaStream_t st = ctx->stream;
+  const long long n = 2 * ctx->N;
+  double bnorm = 0.0;
+  if (int rc = ocp_vec_nrm2(ctx, n, b, &bnorm)) return rc;
+  const double threshold = std::max(rel_tol * bnorm, abs_tol);   // krylov.py:58
+  const double beta = bnorm;                                       // r = M b = b
+  int hist_len = 0;
+  history[hist_len++] = beta;
+  if (!std::isfinite(beta)) return fail(ctx, OCP_ERR_GMRES_BREAKDOWN, "nonfinite initial residual");
+  CK(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+  if (beta <= threshold) {
+    *iters_out = 0; *resid_out = beta; *conv_out = 1;
+    CK(cudaStreamSynchronize(st));
+    return OCP_OK;
+  }
+  // basis Q: the reference grows an (n, cap+1) array by doubling
+  // (krylov.py:89-107); here one grow-only device buffer is kept by the
+  // context (doubling too), so repeated solves do not reallocate
+  auto ensure = [&](long long cols) -> bool {
+    if (cols <= ctx->gm_cols) return true;
+    long long ncols = std::max(cols, 2 * ctx->gm_cols);
+    double* Q2 = nullptr;
+    cudaStreamSynchronize(st);
+    if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess) return false;
+    if (ctx->gm_Q) cudaFree(ctx->gm_Q);
+    ctx->gm_Q = Q2;
+    ctx->gm_cols = ncols;
+    return true;
+  };
+  if (!ctx->gm_w && cudaMalloc(&ctx->gm_w, (size_t)n * sizeof(double)) != cudaSuccess)
+    return fail(ctx, OCP_ERR_CUDA, "GMRES work vector allocation failed");
+  int cap = std::min(32, max_iters);
+  if (!ensure(cap + 1)) return fail(ctx, OCP_ERR_CUDA, "GMRES basis allocation failed");
+  double* Q = ctx->gm_Q;
+  double* w = ctx->gm_w;
+  auto cleanup = [&]() {};
+  k_div<<<ew_grid(n), 256, 0, st>>>(n, b, beta, Q);   // q0 = r0 / beta
+  ++ctx->launches;
+  std::vector<double> cs, sn, g(max_iters + 1, 0.0), h(max_iters + 2);
+  std::vector<std::vector<double>> cols;
+  g[0] = beta;
+  double residual = beta;
+  bool converged = false;
+  int j = 0;
+  for (j = 0; j < max_iters; ++j) {
+    if (j + 1 > cap) {
+      const int ncap = std::min(2 * cap, max_iters);
+      if (ncap + 1 > ctx->gm_cols) {
+        // grow, keeping the first j+1 columns
+        double* Q2 = nullptr;
+        const long long ncols = std::max<long long>(ncap + 1, 2 * ctx->gm_cols);
+        cudaStreamSynchronize(st);
+        if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess)
+          return fail(ctx, OCP_ERR_CUDA, "GMRES basis growth failed");
+        cudaMemcpyAsync(Q2, Q, (size_t)(j + 1) * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+        cudaStreamSynchronize(st);
+        cudaFree(ctx->gm_Q);
+        ctx->gm_Q = Q = Q2;
+        ctx->gm_cols = ncols;
+      }
+      cap = ncap;
+    }
+    if (int rc = ocp_raspen_jvp(ctx, fac, Q + (long long)j * n, w)) { cleanup(); return rc; }
+    if (int rc = ocp_arnoldi(ctx, n, Q, n, j, w, h.data())) { cleanup(); return rc; }
+    for (int i = 0; i <= j + 1; ++i)
+      if (!std::isfinite(h[i])) {
+        cleanup();
+        return fail(ctx, OCP_ERR_GMRES_BREAKDOWN, "nonfinite Arnoldi entries at iteration %d", j + 1);
+      }
+    double hmax = 0.0;
+    for (int i = 0; i <= j; ++i) hmax = std::max(hmax, std::fabs(h[i]));
+    const bool happy = h[j + 1] <= 1e-14 * std::max(1.0, hmax);   // krylov.py:120
+    for (int i = 0; i < j; ++i) {                                   // krylov.py:124-127
+      const double hi = cs[i] * h[i] + sn[i] * h[i + 1];
+      h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+      h[i] = hi;
+    }
+    const double rad = std::hypot(h[j], h[j + 1]);
+    double c = 1.0, sv = 0.0;
+    if (rad != 0.0) { c = h[j] / rad; sv = h[j + 1] / rad; }
+    cs.push_back(c);
+    sn.push_back(sv);
+    h[j] = rad;
+    g[j + 1] = -sv * g[j];
+    g[j] = c * g[j];
+    cols.emplace_back(h.begin(), h.begin() + j + 1);
+    residual = std::fabs(g[j + 1]);
+    history[hist_len++] = residual;
+    if (residual <= threshold || happy) {
+      converged = true;
+      break;
+    }
+  }
+  const int steps = std::min(j + 1, max_iters);
+  // back substitution (krylov.py:145-150)
+  std::vector<double> y(steps, 0.0);
+  for (int i = steps - 1; i >= 0; --i) {
+    double dot = 0.0;
+    for (int k = i + 1; k < steps; ++k) dot += cols[k][i] * y[k];
+    y[i] = (g[i] - dot) / cols[i][i];
+  }
+  int rc = ocp_gemv_add(ctx, n, Q, n, steps, y.data(), x, x);
+  cleanup();
+  if (rc) return rc;
+  *iters_out = steps;
+  *resid_out = residual;
+  *conv_out = converged ? 1 : 0;
   return OCP_OK;
 }
 

@@ -268,6 +268,45 @@ def raspen_solve(x0, dec, spec, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8
     return x.to_host(), report
 
 
+class _RaspenOperator:
+    """Jacobian action of the fixed-point residual at one iterate (schwarz.py:384-395).
+
+    Callable on device vectors (generic GMRES) and with a fused native GMRES
+    for the unpreconditioned, unrestarted solve raspen_solve performs.
+    """
+
+    def __init__(self, engine, fac, state, corr):
+        self.engine, self.fac, self.state, self.corr = engine, fac, state, corr
+
+    def _check(self):
+        if self.state["corr"] is not self.corr:
+            raise RuntimeError("stale corrections: a newer iterate was evaluated")
+
+    def __call__(self, d):
+        self._check()
+        return _jvp(self.engine, self.fac, d)
+
+    def fused_gmres(self, b, cfg):
+        from .krylov import GmresBreakdownError, GmresResult
+        self._check()
+        e = self.engine
+        x = e.vector(b.n)
+        iters = nat.ctypes.c_int()
+        conv = nat.ctypes.c_int()
+        resid = nat.ctypes.c_double()
+        hist = np.zeros(cfg.max_iters + 1)
+        rc = e.lib.ocp_raspen_gmres(
+            e.ctx, nat.ctypes.c_void_p(self.fac.addr), b.ptr, float(cfg.rel_tol),
+            float(cfg.abs_tol), int(cfg.max_iters), x.ptr, nat.ctypes.byref(iters),
+            nat.ctypes.byref(resid), nat.ctypes.byref(conv),
+            hist.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_double)))
+        if rc == nat.OCP_ERR_GMRES_BREAKDOWN:
+            raise GmresBreakdownError(e.error())
+        e.check(rc, "ocp_raspen_gmres")
+        k = iters.value
+        return GmresResult(x, k, resid.value, bool(conv.value), list(hist[:k + 1]))
+
+
 def solve_on_device(engine, x0, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8,
                     inner_max_outer=200, continuation=True, backtracking=False):
     """raspen_solve on a device-resident x0; returns (x DeviceVector or None on failure, report)."""
@@ -300,12 +339,7 @@ def solve_on_device(engine, x0, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8
         if corr is None or corr["eps"] != eps or not corr["x"].equals(x):
             raise RuntimeError("Jacobian requested before a residual evaluation at this iterate")
 
-        def apply(d):
-            if state["corr"] is not corr:
-                raise RuntimeError("stale corrections: a newer iterate was evaluated")
-            return _jvp(engine, fac, d)
-
-        return apply
+        return _RaspenOperator(engine, fac, state, corr)
 
     outer_cfg = NewtonConfig(tol=cfg.tol, max_outer=cfg.max_outer,
                              sigma=cfg.sigma if backtracking else math.inf,

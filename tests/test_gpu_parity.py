@@ -290,3 +290,28 @@ def test_local_failure_becomes_failed_report_and_solve_is_deterministic():
     np.testing.assert_array_equal(xa, xb)
     assert ra.residual_norms == rb.residual_norms
     assert len(ra.inner_iters) == ra.outer_iters + 1 and set(ra.alphas) == {1.0}
+
+
+def test_fused_native_gmres_matches_python_gmres():
+    """The native GMRES (ocp_raspen_gmres) and the Python device GMRES run the
+    same algorithm on the same operator: same iteration count, history to
+    rounding, solution to 1e-12."""
+    from paper_2411_00546_b200 import gmres
+    from paper_2411_00546_b200.schwarz import _RaspenOperator, _sweep
+    tag, n, s1, s2, m, phi, nu, mu = UNIT_CASES[1]
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, s1, s2, m)
+    eng = build_local_systems(dec, spec)
+    rng = np.random.default_rng(7)
+    xd = eng.from_host(0.2 * rng.standard_normal(2 * n * n))
+    fac = eng.factor_store()
+    fval, _ = _sweep(eng, xd, fac, ContinuationSchedule.fixed(1e-2), NewtonConfig(tol=1e-10))
+    state = {"corr": "c"}
+    op = _RaspenOperator(eng, fac, state, "c")
+    b = fval.scaled(-1.0)
+    cfg = KrylovConfig(rel_tol=1e-10, max_iters=200)
+    r1 = gmres(op, b, cfg)
+    r2 = op.fused_gmres(b, cfg)
+    assert r1.converged and r2.converged and r1.iters == r2.iters
+    np.testing.assert_allclose(r2.history, r1.history, rtol=1e-10)
+    assert rel_l2(r2.x.to_host(), r1.x.to_host()) <= 1e-12
