@@ -197,9 +197,12 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
   extern __shared__ __align__(16) double sm[];
   __shared__ int bad;
   __shared__ double rd[2][16];  // reciprocal pivots of U_aa, U_cc
+  __shared__ double Pn[16 * LDP];   // next panel's A_aa, factored ahead (lookahead)
+  __shared__ double rdn[16];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = LU_THREADS / 32;
   constexpr int SIDE = NW - 1;  // forms the block inverses at the start of the update phase
+  constexpr int LAW = 0;        // lookahead warp: factors the next panel's A_aa during the update
   double* win = scratch + (long long)blockIdx.x * ws_stride;
   for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
     const int sid = list[li];
@@ -240,6 +243,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
             const int r = r0 + q * NW, i = k0 + r;
             if (r < W + NBF) {
               if (i >= fresh || k0 + lane >= fresh) v[q] = entry(s, row_info(s, JD, i), k0 + lane, off);
+              if (K > 0 && r < 16 && lane < 16) v[q] = Pn[r * LDP + lane];  // factored ahead
               P[r * LDP + lane] = v[q];
             }
           }
@@ -266,8 +270,13 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
         }
       }
       __syncthreads();
-      // ---- 2a. LU(A_aa) (warp 0)
-      if (warp == 0) warp_lu16(P, 0, lane, rd[0], &bad);
+      // ---- 2a. LU(A_aa) (warp 0); from the second panel on it was factored
+      //          during the previous update phase (lookahead warp)
+      if (K == 0) {
+        if (warp == 0) warp_lu16(P, 0, lane, rd[0], &bad);
+      } else if (tid < 16) {
+        rd[0][tid] = rdn[tid];
+      }
       __syncthreads();
       PHASE_MARK(2);
       // ---- 2b. L_ba, X_a (rows 16..W+31, cols 0..15) solve against U_aa;
@@ -405,7 +414,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
         const int g = lane >> 2, t4 = lane & 3;
         const int TR = (W + 31) >> 5, TC = W >> 4;     // last tile row may be 16 rows
         const int fresh = K == 0 ? k0 : k0 + W;        // indices >= fresh never updated
-        for (int wt = (warp + 1) & (NW - 1); wt < TR * TC; wt += NW) {
+        for (int wt = warp; wt < TR * TC; wt += NW) {
           const int tr = wt / TC, tc = wt - tr * TC;
           const int R0 = 32 * tr, C0 = 16 * tc;
           const int mrows = (W - R0) >= 32 ? 4 : 2;    // 8-row slabs in this tile
@@ -462,6 +471,18 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
             for (int ni = 0; ni < 2; ++ni)
               if (mi < mrows)
                 *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
+          if (warp == LAW && wt == 0 && K + 1 < nblk) {
+            // tile 0 holds the next panel's A_aa (rows/cols [k0+32, k0+48)),
+            // now final: factor it here, overlapped with the other warps' update
+            __syncwarp();
+            for (int e = lane; e < 256; e += 32) {
+              const int r = e >> 4, cc = e & 15;
+              int pr = ks + NBF + r; pr -= pr >= WS ? WS : 0;
+              int pc = ks + NBF + cc; pc -= pc >= WS ? WS : 0;
+              Pn[r * LDP + cc] = win[(long long)pr * WS + pc];
+            }
+            warp_lu16(Pn, 0, lane, rdn, &bad);
+          }
         }
       }
       // ---- 3c. the rest of the finished 32-block -> factor store
