@@ -199,6 +199,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
   __shared__ double rd[2][16];  // reciprocal pivots of U_aa, U_cc
   __shared__ double Pn[16 * LDP];   // next panel's A_aa, factored ahead (lookahead)
   __shared__ double rdn[16];
+  __shared__ int tile_ctr;          // dynamic tile scheduler of the update phase
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = LU_THREADS / 32;
   constexpr int SIDE = NW - 1;  // forms the block inverses at the start of the update phase
@@ -344,6 +345,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       __syncthreads();
       PHASE_MARK(4);
       // ---- 2d. X_b solve against U_cc (rows 32..), Y_b against L_cc (U rows 16..31)
+      if (tid == 0) tile_ctr = 1;   // tile 0 belongs to the lookahead warp
       for (int task = tid; task < 2 * W; task += LU_THREADS) {
         if (task < W) row_solve_u(P + (NBF + task) * LDP + 16, P, 16, rd[1]);
         else col_solve_l(U + 16 * LDU + (task - W), LDU, P, 16);
@@ -414,7 +416,16 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
         const int g = lane >> 2, t4 = lane & 3;
         const int TR = (W + 31) >> 5, TC = W >> 4;     // last tile row may be 16 rows
         const int fresh = K == 0 ? k0 : k0 + W;        // indices >= fresh never updated
-        for (int wt = warp; wt < TR * TC; wt += NW) {
+        // dynamic tile scheduling: the lookahead warp takes tile 0 first, the
+        // side warp starts with the inverses; everybody then pulls tiles
+        int wt = warp == LAW ? 0 : -1;
+        for (;;) {
+          if (wt < 0) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&tile_ctr, 1);
+            wt = __shfl_sync(0xffffffffu, t, 0);
+          }
+          if (wt >= TR * TC) break;
           const int tr = wt / TC, tc = wt - tr * TC;
           const int R0 = 32 * tr, C0 = 16 * tc;
           const int mrows = (W - R0) >= 32 ? 4 : 2;    // 8-row slabs in this tile
@@ -483,6 +494,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
             }
             warp_lu16(Pn, 0, lane, rdn, &bad);
           }
+          wt = -1;
         }
       }
       // ---- 3c. the rest of the finished 32-block -> factor store
