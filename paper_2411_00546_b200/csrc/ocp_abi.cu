@@ -65,6 +65,10 @@ struct ocp_ctx {
   double* gm_Q = nullptr;      // persistent GMRES basis (grow-only), ocp_raspen_gmres
   double* gm_w = nullptr;
   long long gm_cols = 0;
+  double* gm_dh = nullptr;     // two device slots of Arnoldi coefficients (pipelined GMRES)
+  double* gm_hh = nullptr;     // their pinned host copies
+  int gm_hcap = 0;             // entries per slot
+  cudaEvent_t gm_ev[2] = {nullptr, nullptr};
   int h_cap = 0;
   cudaStream_t stream = nullptr;
   // pinned host staging
@@ -452,12 +456,14 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
                   (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
-                  (void*)ctx->gm_Q, (void*)ctx->gm_w,
+                  (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
-                  (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags})
+                  (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
+                  (void*)ctx->gm_hh})
     if (p) cudaFreeHost(p);
+  for (auto e : ctx->gm_ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pending) {
     cudaEventDestroy(e.a);
     cudaEventDestroy(e.b);
@@ -934,42 +940,86 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double re
   };
   if (!ctx->gm_w && cudaMalloc(&ctx->gm_w, (size_t)n * sizeof(double)) != cudaSuccess)
     return fail(ctx, OCP_ERR_CUDA, "GMRES work vector allocation failed");
-  int cap = std::min(32, max_iters);
-  if (!ensure(cap + 1)) return fail(ctx, OCP_ERR_CUDA, "GMRES basis allocation failed");
+  // Arnoldi coefficient slots: step j writes slot j&1 on the device, copies it
+  // to pinned host memory and records gm_ev[j&1]
+  if (ctx->gm_hcap < max_iters + 2) {
+    cudaStreamSynchronize(st);
+    if (ctx->gm_dh) cudaFree(ctx->gm_dh);
+    if (ctx->gm_hh) cudaFreeHost(ctx->gm_hh);
+    ctx->gm_dh = nullptr; ctx->gm_hh = nullptr; ctx->gm_hcap = 0;
+    if (cudaMalloc(&ctx->gm_dh, 2 * (size_t)(max_iters + 2) * sizeof(double)) != cudaSuccess ||
+        cudaMallocHost(&ctx->gm_hh, 2 * (size_t)(max_iters + 2) * sizeof(double)) != cudaSuccess)
+      return fail(ctx, OCP_ERR_CUDA, "GMRES coefficient buffers");
+    ctx->gm_hcap = max_iters + 2;
+  }
+  for (auto& e : ctx->gm_ev)
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return fail(ctx, OCP_ERR_CUDA, "GMRES events");
+  const int hs = ctx->gm_hcap;
+  if (!ensure(std::min(32, max_iters) + 2)) return fail(ctx, OCP_ERR_CUDA, "GMRES basis allocation failed");
   double* Q = ctx->gm_Q;
   double* w = ctx->gm_w;
   auto cleanup = [&]() {};
   k_div<<<ew_grid(n), 256, 0, st>>>(n, b, beta, Q);   // q0 = r0 / beta
   ++ctx->launches;
+  // One Arnoldi step (JVP + MGS) is always queued ahead of the host's Givens
+  // update: step j+1 is enqueued before step j's coefficients are inspected,
+  // so the device never idles on the host round trip.  When step j converges
+  // the speculative step j+1 is discarded (it only wrote basis column j+2 and
+  // slot (j+1)&1); decisions and results are those of the sequential loop.
+  bool pipelined = true;
+  auto enqueue = [&](int jj) -> int {
+    if (jj + 2 > ctx->gm_cols) {   // grow, keeping the first jj+1 columns (stream-ordered copy)
+      double* Q2 = nullptr;
+      const long long ncols = std::max<long long>(jj + 2, 2 * ctx->gm_cols);
+      cudaStreamSynchronize(st);
+      if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess)
+        return fail(ctx, OCP_ERR_CUDA, "GMRES basis growth failed");
+      cudaMemcpyAsync(Q2, Q, (size_t)(jj + 1) * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      cudaStreamSynchronize(st);
+      cudaFree(ctx->gm_Q);
+      ctx->gm_Q = Q = Q2;
+      ctx->gm_cols = ncols;
+    }
+    if (int rc = ocp_raspen_jvp(ctx, fac, Q + (long long)jj * n, w)) return rc;
+    double* dh = ctx->gm_dh + (jj & 1) * hs;
+    if (pipelined) {
+      Timer t(ctx, CLS_MGS);
+      cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, n, jj, w, ctx->red_partials, dh);
+      if (e == cudaSuccess) {
+        ++ctx->launches;
+      } else if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        pipelined = false;
+      } else {
+        return fail(ctx, OCP_ERR_CUDA, "cooperative Arnoldi launch: %s", cudaGetErrorString(e));
+      }
+    }
+    if (!pipelined) {   // per-pass kernels (vectors too large for the cooperative kernel)
+      if (int rc = ocp_arnoldi(ctx, n, Q, n, jj, w, ctx->gm_hh + (jj & 1) * hs)) return rc;
+    } else {
+      CK(cudaMemcpyAsync(ctx->gm_hh + (jj & 1) * hs, dh, (jj + 2) * sizeof(double),
+                         cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaEventRecord(ctx->gm_ev[jj & 1], st));
+    return OCP_OK;
+  };
   std::vector<double> cs, sn, g(max_iters + 1, 0.0), h(max_iters + 2);
   std::vector<std::vector<double>> cols;
   g[0] = beta;
   double residual = beta;
   bool converged = false;
   int j = 0;
+  if (int rc = enqueue(0)) return rc;
   for (j = 0; j < max_iters; ++j) {
-    if (j + 1 > cap) {
-      const int ncap = std::min(2 * cap, max_iters);
-      if (ncap + 1 > ctx->gm_cols) {
-        // grow, keeping the first j+1 columns
-        double* Q2 = nullptr;
-        const long long ncols = std::max<long long>(ncap + 1, 2 * ctx->gm_cols);
-        cudaStreamSynchronize(st);
-        if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess)
-          return fail(ctx, OCP_ERR_CUDA, "GMRES basis growth failed");
-        cudaMemcpyAsync(Q2, Q, (size_t)(j + 1) * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
-        cudaStreamSynchronize(st);
-        cudaFree(ctx->gm_Q);
-        ctx->gm_Q = Q = Q2;
-        ctx->gm_cols = ncols;
-      }
-      cap = ncap;
-    }
-    if (int rc = ocp_raspen_jvp(ctx, fac, Q + (long long)j * n, w)) { cleanup(); return rc; }
-    if (int rc = ocp_arnoldi(ctx, n, Q, n, j, w, h.data())) { cleanup(); return rc; }
+    if (j + 1 < max_iters && pipelined)
+      if (int rc = enqueue(j + 1)) { cleanup(); return rc; }
+    CK(cudaEventSynchronize(ctx->gm_ev[j & 1]));
+    std::copy(ctx->gm_hh + (j & 1) * hs, ctx->gm_hh + (j & 1) * hs + j + 2, h.begin());
     for (int i = 0; i <= j + 1; ++i)
       if (!std::isfinite(h[i])) {
         cleanup();
+        cudaStreamSynchronize(st);
         return fail(ctx, OCP_ERR_GMRES_BREAKDOWN, "nonfinite Arnoldi entries at iteration %d", j + 1);
       }
     double hmax = 0.0;
@@ -995,6 +1045,8 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double re
       converged = true;
       break;
     }
+    if (!pipelined && j + 1 < max_iters)
+      if (int rc = enqueue(j + 1)) { cleanup(); return rc; }
   }
   const int steps = std::min(j + 1, max_iters);
   // back substitution (krylov.py:145-150)

@@ -280,22 +280,16 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       }
       __syncthreads();
       PHASE_MARK(2);
-      // ---- 2b. L_ba, X_a (rows 16..W+31, cols 0..15) solve against U_aa;
-      //          U_ab (rows 0..15, cols 16..31), Y_a (U rows 0..15) against L_aa
-      for (int task = tid; task < 2 * (W + 16); task += LU_THREADS) {
-        if (task < W + 16) {
-          row_solve_u(P + (16 + task) * LDP, P, 0, rd[0]);
-        } else {
-          const int c = task - (W + 16);
-          if (c < 16) col_solve_l(P + 16 + c, LDP, P, 0);
-          else col_solve_l(U + (c - 16), LDU, P, 0);
-        }
-      }
-      __syncthreads();
-      PHASE_MARK(3);
-      // ---- 2c. warp 0: S = A_bb - L_ba U_ab, LU(S);
-      //          warps 1..7: A21_b -= X_a U_ab (rows 32..), A12_b -= L_ba Y_a
+      // ---- 2b/2c. warp 0: L_ba, U_ab (the 16x16 blocks next to A_aa), then
+      //          S = A_bb - L_ba U_ab and LU(S), announcing L_ba/U_ab on named
+      //          barrier 1 before the serial LU(S);
+      //          warps 1..7: X_a (rows 32..) against U_aa, Y_a (U rows 0..15)
+      //          against L_aa, then (after barrier 1) A21_b -= X_a U_ab and
+      //          A12_b -= L_ba Y_a, overlapped with LU(S)
       if (warp == 0) {
+        if (lane < 16) row_solve_u(P + (16 + lane) * LDP, P, 0, rd[0]);
+        else col_solve_l(P + lane, LDP, P, 0);
+        __syncwarp();
         if (lane < 16) {
           double* row = P + (16 + lane) * LDP + 16;
           double a[16];
@@ -310,9 +304,14 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
 #pragma unroll
           for (int j = 0; j < 16; ++j) row[j] = a[j];
         }
-        __syncwarp();
+        asm volatile("bar.arrive 1, %0;" :: "n"(LU_THREADS) : "memory");
         warp_lu16(P, 16, lane, rd[1], &bad);
       } else {
+        for (int task = tid - 32; task < 2 * W; task += LU_THREADS - 32) {
+          if (task < W) row_solve_u(P + (NBF + task) * LDP, P, 0, rd[0]);
+          else col_solve_l(U + (task - W), LDU, P, 0);
+        }
+        asm volatile("bar.sync 1, %0;" :: "n"(LU_THREADS) : "memory");
         for (int task = tid - 32; task < 2 * W; task += LU_THREADS - 32) {
           if (task < W) {  // row 32+task: cols 16..31 -= X_a[row] U_ab
             double* row = P + (NBF + task) * LDP;

@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include "ocp_kernels.cuh"
+#include "ocp_tma.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -90,11 +91,133 @@ k_arnoldi(long long n, const double* __restrict__ Q, long long ldq, int j,
   }
 }
 
+// Double-buffered variant for vectors whose per-SM share fits twice in shared
+// memory (config 4: 2 x 110 KB): block b owns the contiguous range
+// [b*per, b*per + per) and thread t its elements t + 512 k.  q_{i+1} streams
+// into the idle buffer by one TMA bulk copy issued at the start of pass i, so
+// the HBM transfer of the next basis vector runs under this pass's barrier and
+// reductions instead of after them (measured: a pass that loads q after the
+// grid barrier costs ~3x the bare HBM stream time).
+template <int CH>
+__global__ void __launch_bounds__(ARN_THREADS, 1)
+k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
+             const double* __restrict__ w_in, double* partials, double* h_out, int per) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double qb[];  // [2][per]
+  __shared__ double red[32];
+  __shared__ __align__(8) uint64_t bars[2];
+  const int tid = threadIdx.x;
+  const long long b0 = (long long)blockIdx.x * per;
+  const int cnt = (int)(n - b0 < per ? (n - b0 > 0 ? n - b0 : 0) : per);
+  const uint32_t bytes = (uint32_t)cnt * 8u;
+  double w[CH];
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int e = tid + k * ARN_THREADS;
+    w[k] = e < cnt ? w_in[b0 + e] : 0.0;
+  }
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && cnt > 0) {
+    mbar_expect_tx(&bars[0], bytes);
+    bulk_g2s(qb, Q + b0, bytes, &bars[0]);
+  }
+  const int nb = gridDim.x;
+  for (int i = 0; i <= j + 1; ++i) {
+    const bool norm_pass = (i == j + 1);
+    const double* cur = qb + (i & 1) * per;
+    double acc = 0.0;
+    if (!norm_pass) {
+      if (cnt > 0) mbar_wait(&bars[i & 1], (i >> 1) & 1);
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int e = tid + k * ARN_THREADS;
+        acc = fma(e < cnt ? cur[e] : 0.0, w[k], acc);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < CH; ++k) acc = fma(w[k], w[k], acc);
+    }
+    // (the barrier inside block_sum_all also retires every read of the other
+    //  buffer from pass i-1, so it can be refilled now)
+    const double bsum = block_sum_all<ARN_THREADS>(acc, red);
+    if (tid == 0 && i + 1 <= j && cnt > 0) {
+      uint64_t* bar = &bars[(i + 1) & 1];
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(qb + ((i + 1) & 1) * per, Q + (long long)(i + 1) * ldq + b0, bytes, bar);
+    }
+    double* part = partials + (i & 1) * nb;
+    if (tid == 0) part[blockIdx.x] = bsum;
+    grid.sync();
+    double v = 0.0;
+    for (int b = tid; b < nb; b += blockDim.x) v += part[b];
+    const double h = block_sum_all<ARN_THREADS>(v, red);
+    if (norm_pass) {
+      const double hn = sqrt(h);
+      if (blockIdx.x == 0 && tid == 0) h_out[i] = hn;
+      double* qn = const_cast<double*>(Q) + (long long)(j + 1) * ldq + b0;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int e = tid + k * ARN_THREADS;
+        if (e < cnt) qn[e] = __ddiv_rn(w[k], hn);
+      }
+    } else {
+      if (blockIdx.x == 0 && tid == 0) h_out[i] = h;
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        const int e = tid + k * ARN_THREADS;
+        w[k] = __dsub_rn(w[k], __dmul_rn(h, e < cnt ? cur[e] : 0.0));
+      }
+    }
+  }
+}
+
+template <int CH>
+static cudaError_t launch_db(cudaStream_t st, int grid, int per, long long n, const double* Q,
+                             long long ldq, int j, const double* w_in, double* partials,
+                             double* h_out) {
+  void* fn = (void*)k_arnoldi_db<CH>;
+  const int smem = 2 * per * (int)sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ARN_THREADS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  void* args[] = {(void*)&n, (void*)&Q, (void*)&ldq, (void*)&j, (void*)&w_in, (void*)&partials,
+                  (void*)&h_out, (void*)&per};
+  return cudaLaunchCooperativeKernel(fn, grid, ARN_THREADS, args, smem, st);
+}
+
 // grid of co-resident blocks; returns cudaErrorNotSupported when n does not
 // fit the register-resident variant (caller falls back to per-pass kernels)
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
                            long long ldq, int j, const double* w_in, double* partials,
                            double* h_out) {
+  // double-buffered variant when the aligned per-SM share fits twice in shared memory
+  {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    long long per = (n + num_sms - 1) / num_sms;
+    per += per & 1;
+    const bool aligned = (n % 2 == 0) && (ldq % 2 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(Q) & 15) == 0);
+    if (aligned && n > 0 && num_sms <= 256 && 16 * per + 512 <= optin && per <= 32 * ARN_THREADS) {
+      const int p = (int)per;
+      cudaError_t e;
+      if (per <= 8 * ARN_THREADS) e = launch_db<8>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      else if (per <= 16 * ARN_THREADS) e = launch_db<16>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      else if (per <= 24 * ARN_THREADS) e = launch_db<24>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      else e = launch_db<32>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      if (e != cudaErrorNotSupported) return e;
+      cudaGetLastError();
+    }
+  }
   const long long threads = (long long)num_sms * ARN_THREADS;
   const long long ch = (n + threads - 1) / threads;
   void* fn = nullptr;
