@@ -148,6 +148,33 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac_dev, const double* b_dev, d
 /* out = x + Q[:, :k] @ y  (krylov.py:151) */
 int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k,
                  const double* y_host, const double* x, double* out);
+/* ---- linear-RAS Newton-Krylov (method newton-ras-eps) -------------------
+ * harness/experiments.py:72-84: monolithic newton_continuation on the global
+ * residual with GMRES left-preconditioned by one-level RAS. */
+/* r = F_eps(x) on the whole grid, check=False  (system.py:147-152) */
+int ocp_global_residual(ocp_ctx* ctx, const double* x_dev, double eps, double* r_dev);
+/* Jacobian of F_eps at x as its per-point diagonals jd_dev[4N] =
+ * (4/h^2 + phi'(y), b12, b21, 0)  (system.py:135-144, 155-160: jacobian()).
+ * OCP_ERR_NONFINITE "phi'(y)@k" / "phi''(y)@k" like the reference's checks. */
+int ocp_global_jacobian(ocp_ctx* ctx, const double* x_dev, double eps, double* jd_dev);
+/* out = J d, the CSR row sums of jacobian(x) @ d  (system.py:155-160) */
+int ocp_global_jvp(ocp_ctx* ctx, const double* jd_dev, const double* d_dev, double* out_dev);
+/* ras_preconditioner build (schwarz.py:221-232): local pair Jacobians at
+ * x[pair_idx] of every subdomain, batched banded LU into fac_dev (a factor
+ * store as for ocp_raspen_residual).  OCP_ERR_LOCAL_SOLVE ("singular local
+ * block") / OCP_ERR_NONFINITE with *failed_sub = subdomain. */
+int ocp_ras_factor(ocp_ctx* ctx, const double* x_dev, double eps, double* fac_dev,
+                   int* failed_sub);
+/* out = sum_i P~_i J_i^-1 R_i v  (the apply closure, schwarz.py:234-239) */
+int ocp_ras_apply(ocp_ctx* ctx, const double* fac_dev, const double* v_dev, double* out_dev);
+/* GMRES on J(x) (jd_dev) left-preconditioned by the RAS factors: the
+ * direction solve of newton.py:115-124 with precond = ras_preconditioner
+ * (krylov.py:44-151: threshold on ||M b||, w = M J q_j).  Same outputs and
+ * status codes as ocp_raspen_gmres. */
+int ocp_ras_gmres(ocp_ctx* ctx, const double* jd_dev, const double* fac_dev, const double* b_dev,
+                  double rel_tol, double abs_tol, int max_iters, double* x_dev, int* iters_host,
+                  double* residual_host, int* converged_host, double* history_host);
+
 /* u = -(p + mu P_eps(-p/mu))/nu  (system.py:173-174) */
 int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps,
                         double* u);

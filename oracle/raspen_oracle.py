@@ -34,6 +34,10 @@ import scipy.sparse.linalg as spla
 EXP_ARG_MAX = 700.0
 
 
+class OracleLinearFailure(RuntimeError):
+    """GMRES did not converge (LinearSolveError, `newton.py:119-123`)."""
+
+
 class OracleLocalFailure(RuntimeError):
     def __init__(self, sub, message):
         self.subdomain = sub
@@ -199,6 +203,8 @@ def newton(x0, F, J_solve, eps0, gamma, eps_min, tol, max_outer, sigma, max_halv
                 (norms, epss, alphas)
         try:
             d = J_solve(x, eps, -r)
+        except OracleLinearFailure as exc:            # newton.py:119-123 (GMRES)
+            return x, False, iters, str(exc), (norms, epss, alphas)
         except RuntimeError as exc:                   # newton.py:126-129
             return x, False, iters, f"sparse factorization failed: {exc}", (norms, epss, alphas)
         alpha, ok = 1.0, False                        # backtrack, newton.py:96-112
@@ -225,8 +231,10 @@ def newton(x0, F, J_solve, eps0, gamma, eps_min, tol, max_outer, sigma, max_halv
 # GMRES (`pkg/src/ocp/krylov.py:44-151`), unrestarted, MGS Arnoldi
 # --------------------------------------------------------------------------
 
-def gmres(apply_op, b, rel_tol, max_iters, abs_tol=0.0):
-    b = np.asarray(b, dtype=float)
+def gmres(apply_op, b, rel_tol, max_iters, abs_tol=0.0, precond=None):
+    """Left-preconditioned when ``precond`` is given (`krylov.py:54-60,110`)."""
+    m = precond if precond is not None else (lambda v: v)
+    b = m(np.asarray(b, dtype=float))
     thr = max(rel_tol * float(np.linalg.norm(b)), abs_tol)
     beta = float(np.linalg.norm(b))
     history = [beta]
@@ -252,7 +260,7 @@ def gmres(apply_op, b, rel_tol, max_iters, abs_tol=0.0):
             grown = np.empty((b.shape[0], cap + 1))
             grown[:, :j + 1] = q[:, :j + 1]
             q = grown
-        w = np.array(apply_op(q[:, j]), dtype=float, copy=True)
+        w = np.array(m(apply_op(q[:, j])), dtype=float, copy=True)
         h = np.empty(j + 2)
         with np.errstate(invalid="ignore", over="ignore"):
             for i in range(j + 1):
@@ -478,6 +486,88 @@ def raspen_solve(prob, x0, eps0, gamma, eps_min, tol=1e-10, max_outer=200,
     return x, rep
 
 
+# --------------------------------------------------------------------------
+# linear-RAS Newton-Krylov, method newton-ras-eps (`harness/experiments.py:72-84`)
+# --------------------------------------------------------------------------
+
+def laplacian(n):
+    """Kron-sum 5-point Laplacian / h^2, CSR with sorted columns (`grid.py:83-91`)."""
+    h2 = (1.0 / (n + 1)) ** 2
+    t = sp.diags([-np.ones(n - 1), 2.0 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1], format="csr")
+    eye = sp.identity(n, format="csr")
+    a = ((sp.kron(eye, t) + sp.kron(t, eye)) / h2).tocsr()
+    a.sort_indices()
+    return a
+
+
+def global_residual(prob, x, eps):
+    """F_eps(x) with check=False (`system.py:118-132,147-152`)."""
+    a = prob.__dict__.get("_lap")
+    if a is None:
+        a = prob._lap = laplacian(prob.n)
+    n2 = prob.n * prob.n
+    y, p = x[:n2], x[n2:]
+    r1, r2 = rows_from_actions(a @ y, a @ p, y, p, prob.f, prob.y_d, prob.phi, prob.nu,
+                               prob.mu, eps)
+    return np.concatenate([r1, r2])
+
+
+def global_jacobian(prob, x, eps):
+    """[[A + diag(phi'), diag(b12)], [diag(b21), A + diag(phi')]] as CSR (`system.py:155-160`)."""
+    a = prob.__dict__.get("_lap")
+    if a is None:
+        a = prob._lap = laplacian(prob.n)
+    n2 = prob.n * prob.n
+    y, p = x[:n2], x[n2:]
+    d1, b12, b21 = jac_diagonals(y, p, prob.phi, prob.nu, prob.mu, eps)
+    a11 = a + sp.diags(d1)
+    return sp.bmat([[a11, sp.diags(b12)], [sp.diags(b21), a11]], format="csr")
+
+
+def ras_preconditioner(prob, x, eps):
+    """One-level RAS at x: SuperLU of every local pair Jacobian at x[pair_idx]
+    (`schwarz.py:221-239`)."""
+    lus = []
+    for i, r in enumerate(prob.rects):
+        _, J = prob.local_fns(i, x)
+        try:
+            lus.append(spla.splu(J(x[r.pair_idx], eps).tocsc()))
+        except RuntimeError as exc:
+            raise OracleLocalFailure(i, f"singular local block: {exc}") from exc
+
+    def apply(v):
+        out = np.zeros_like(v)
+        for r, lu in zip(prob.rects, lus):
+            w = lu.solve(v[r.pair_idx])
+            out[r.pair_own] = w[r.pair_own_in_local]
+        return out
+
+    return apply
+
+
+def newton_ras_solve(prob, x0, eps0, gamma, eps_min, tol=1e-10, max_outer=200, sigma=1.1,
+                     gmres_rel=1e-8, gmres_max=2000, max_halvings=30):
+    """Monolithic damped Newton with eps-continuation, GMRES directions
+    left-preconditioned by RAS rebuilt at every iterate (`newton.py:133-181`)."""
+    gm = []
+
+    def J_solve(x, eps, rhs):
+        jac = global_jacobian(prob, x, eps)
+        d, k, res, conv, _ = gmres(lambda v: jac @ v, rhs, gmres_rel, gmres_max,
+                                   precond=ras_preconditioner(prob, x, eps))
+        if not conv:
+            raise OracleLinearFailure(f"GMRES stalled at residual {res:.3e} after {k} iterations")
+        gm.append(k)
+        return d
+
+    x, ok, iters, failure, (norms, epss, alphas) = newton(
+        x0, lambda v, e: global_residual(prob, v, e), J_solve, eps0, gamma, eps_min, tol,
+        max_outer, sigma, max_halvings)
+    return x, {"converged": ok, "outer_iters": iters, "failure": failure,
+               "residual_norms": norms, "eps_values": epss, "alphas": alphas,
+               "gmres_iters": gm}
+
+
 def recover_control(p, mu, nu, eps):
     """u = -(p + mu P_eps(-p/mu))/nu (`system.py:173-174`)."""
     return -(p + mu * p_eps(-p / mu, eps)) / nu
@@ -497,5 +587,7 @@ def sample_subdomains(prob, count, seed=0):
 
 
 __all__ = ["Problem", "raspen_residual", "raspen_jvp", "raspen_solve", "gmres", "newton",
+           "global_residual", "global_jacobian", "ras_preconditioner", "newton_ras_solve",
+           "laplacian", "OracleLinearFailure",
            "recover_control", "decompose", "tile_edges", "OracleLocalFailure",
            "dof_updates", "sample_subdomains", "p_eps", "dp_eps", "math"]

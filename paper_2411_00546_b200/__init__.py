@@ -20,3 +20,5 @@ from .schwarz import (CorrectionSet, Decomposition, LocalSolveError, Subdomain,
                       raspen_jacobian_apply, raspen_residual, raspen_solve)
 from .engine import DeviceVector, Engine
 from ._native import NativeError, NativeUnavailable
+from .linear_ras import (GlobalJacobian, RasPreconditioner, global_jacobian, global_residual,
+                         newton_ras_solve, ras_precondition, ras_preconditioner)

@@ -60,6 +60,12 @@ SIGNATURES = {
     "ocp_mgs": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
     "ocp_arnoldi": [_vp, _ll, _vp, _ll, _i, _vp, _c_dbl_p],
     "ocp_raspen_gmres": [_vp, _vp, _vp, _d, _d, _i, _vp, _c_int_p, _c_dbl_p, _c_int_p, _c_dbl_p],
+    "ocp_global_residual": [_vp, _vp, _d, _vp],
+    "ocp_global_jacobian": [_vp, _vp, _d, _vp],
+    "ocp_global_jvp": [_vp, _vp, _vp, _vp],
+    "ocp_ras_factor": [_vp, _vp, _d, _vp, _c_int_p],
+    "ocp_ras_apply": [_vp, _vp, _vp, _vp],
+    "ocp_ras_gmres": [_vp, _vp, _vp, _vp, _d, _d, _i, _vp, _c_int_p, _c_dbl_p, _c_int_p, _c_dbl_p],
     "ocp_gemv_add": [_vp, _ll, _vp, _ll, _i, _c_dbl_p, _vp, _vp],
     "ocp_recover_control": [_vp, _ll, _vp, _d, _vp],
     "ocp_set_profiling": [_vp, _i],

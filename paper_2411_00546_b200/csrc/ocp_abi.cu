@@ -69,6 +69,8 @@ struct ocp_ctx {
   double* gm_hh = nullptr;     // their pinned host copies
   int gm_hcap = 0;             // entries per slot
   cudaEvent_t gm_ev[2] = {nullptr, nullptr};
+  double* gm_t = nullptr;      // J q_j of the preconditioned (linear-RAS) operator
+  unsigned long long* d_gbad = nullptr;   // first nonfinite phi'/phi'' of the global Jacobian
   int h_cap = 0;
   cudaStream_t stream = nullptr;
   // pinned host staging
@@ -456,7 +458,8 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
                   (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
-                  (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh,
+                  (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
+                  (void*)ctx->d_gbad,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
@@ -903,18 +906,115 @@ int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j, cons
   return OCP_OK;
 }
 
-// GMRES for the RASPEN operator, the whole solve in native code
-// (krylov.py:44-151 with precond = None, x0 = None, restart = None).
-int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double rel_tol,
-                     double abs_tol, int max_iters, double* x, int* iters_out, double* resid_out,
-                     int* conv_out, double* history) {
-  if (!ctx || !fac || !b || !x || max_iters < 1) return fail(ctx, OCP_ERR_ARG, "bad argument");
+// Linear-RAS Newton-Krylov (newton-ras-eps): whole-grid residual / Jacobian
+// and the one-level RAS preconditioner built from the batched banded LU.
+int ocp_global_residual(ocp_ctx* ctx, const double* x, double eps, double* r) {
+  if (!ctx || !x || !r) return fail(ctx, OCP_ERR_ARG, "null argument");
+  k_global_residual<<<ew_grid(ctx->N), 256, 0, ctx->stream>>>(ctx->P, x, ctx->d_f, ctx->d_yd, eps, r);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_global_jacobian(ocp_ctx* ctx, const double* x, double eps, double* jd) {
+  if (!ctx || !x || !jd) return fail(ctx, OCP_ERR_ARG, "null argument");
+  cudaStream_t st = ctx->stream;
+  if (!ctx->d_gbad) CK(cudaMalloc(&ctx->d_gbad, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(ctx->d_gbad, 0xff, sizeof(unsigned long long), st));
+  k_global_jacdiag<<<ew_grid(ctx->N), 256, 0, st>>>(ctx->P, x, eps, reinterpret_cast<double4*>(jd),
+                                                     ctx->d_gbad);
+  CKL();
+  unsigned long long bad = 0;
+  CK(cudaMemcpyAsync(&bad, ctx->d_gbad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad != ~0ull)
+    return fail(ctx, OCP_ERR_NONFINITE, "%s@%lld", (bad >> 32) ? "phi''(y)" : "phi'(y)",
+                (long long)(bad & 0xffffffffull));
+  return OCP_OK;
+}
+
+int ocp_global_jvp(ocp_ctx* ctx, const double* jd, const double* d, double* out) {
+  if (!ctx || !jd || !d || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
+  k_global_jvp<<<ew_grid(ctx->N), 256, 0, ctx->stream>>>(ctx->P, reinterpret_cast<const double4*>(jd),
+                                                          d, out);
+  CKL();
+  return OCP_OK;
+}
+
+// local Jacobians at x restricted to every subdomain, factored into fac
+// (ras_preconditioner, schwarz.py:221-232)
+int ocp_ras_factor(ocp_ctx* ctx, const double* x, double eps, double* fac, int* failed_sub) {
+  if (!ctx || !x || !fac) return fail(ctx, OCP_ERR_ARG, "null argument");
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  if (failed_sub) *failed_sub = -1;
+  k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->B);
+  CKL();
+  k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->B, eps, ctx->JD, ctx->d_bad);
+  CKL();
+  std::vector<int> all(I);
+  for (int i = 0; i < I; ++i) all[i] = i;
+  if (int rc = launch_factor(ctx, ctx->d_list_all, all, fac)) return rc;
+  CK(cudaMemcpyAsync(ctx->h_bad, ctx->d_bad, I * sizeof(long long), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int i = 0; i < I; ++i) {
+    if (ctx->h_bad[i] >= 0) {
+      const long long b = ctx->h_bad[i];
+      if (failed_sub) *failed_sub = i;
+      return fail(ctx, OCP_ERR_NONFINITE, "%s@%lld", (b >> 32) ? "phi''(y)" : "phi'(y)",
+                  b & 0xffffffffLL);
+    }
+    if (ctx->h_status[i]) {
+      if (failed_sub) *failed_sub = i;
+      return fail(ctx, OCP_ERR_LOCAL_SOLVE,
+                  "singular local block: zero pivot in banded LU");
+    }
+  }
+  return OCP_OK;
+}
+
+// out = sum_i P~_i J_i^{-1} R_i v  (the apply closure, schwarz.py:234-239)
+int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out) {
+  if (!ctx || !fac || !v || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, v, ctx->B);
+  CKL();
+  {
+    double bytes = 0;
+    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
+    Timer t(ctx, CLS_SOLVE, 0, bytes);
+    CK(launch_band_solve(1, I, st, ctx->d_subs, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B,
+                         ctx->maxW));
+    ++ctx->launches;
+  }
+  k_ras_out<<<dim3(I, 4), 256, 0, st>>>(ctx->d_subs, ctx->P, ctx->B, out);
+  CKL();
+  return OCP_OK;
+}
+
+// GMRES, the whole solve in native code (krylov.py:44-151 with x0 = None,
+// restart = None).  kind 0: the RASPEN Jacobian action from stored factors,
+// no preconditioner; kind 1: J(x) from its diagonals, left-preconditioned by
+// one-level RAS (w = M J q_j, threshold on ||M b||).
+static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* jd, const double* b,
+                      double rel_tol, double abs_tol, int max_iters, double* x, int* iters_out,
+                      double* resid_out, int* conv_out, double* history) {
+  if (!ctx || !fac || !b || !x || max_iters < 1 || (kind == 1 && !jd))
+    return fail(ctx, OCP_ERR_ARG, "bad argument");
   cudaStream_t st = ctx->stream;
   const long long n = 2 * ctx->N;
+  if (kind == 1 && !ctx->gm_t && cudaMalloc(&ctx->gm_t, (size_t)n * sizeof(double)) != cudaSuccess)
+    return fail(ctx, OCP_ERR_CUDA, "GMRES work vector allocation failed");
+  const double* r0 = b;
+  if (kind == 1) {   // mb = M b (krylov.py:55-60)
+    if (int rc = ocp_ras_apply(ctx, fac, b, ctx->gm_t)) return rc;
+    r0 = ctx->gm_t;
+  }
   double bnorm = 0.0;
-  if (int rc = ocp_vec_nrm2(ctx, n, b, &bnorm)) return rc;
+  if (int rc = ocp_vec_nrm2(ctx, n, r0, &bnorm)) return rc;
   const double threshold = std::max(rel_tol * bnorm, abs_tol);   // krylov.py:58
-  const double beta = bnorm;                                       // r = M b = b
+  const double beta = bnorm;                                       // r = M b
   int hist_len = 0;
   history[hist_len++] = beta;
   if (!std::isfinite(beta)) return fail(ctx, OCP_ERR_GMRES_BREAKDOWN, "nonfinite initial residual");
@@ -960,7 +1060,7 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double re
   double* Q = ctx->gm_Q;
   double* w = ctx->gm_w;
   auto cleanup = [&]() {};
-  k_div<<<ew_grid(n), 256, 0, st>>>(n, b, beta, Q);   // q0 = r0 / beta
+  k_div<<<ew_grid(n), 256, 0, st>>>(n, r0, beta, Q);   // q0 = r0 / beta
   ++ctx->launches;
   // One Arnoldi step (JVP + MGS) is always queued ahead of the host's Givens
   // update: step j+1 is enqueued before step j's coefficients are inspected,
@@ -981,7 +1081,12 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double re
       ctx->gm_Q = Q = Q2;
       ctx->gm_cols = ncols;
     }
-    if (int rc = ocp_raspen_jvp(ctx, fac, Q + (long long)jj * n, w)) return rc;
+    if (kind == 0) {
+      if (int rc = ocp_raspen_jvp(ctx, fac, Q + (long long)jj * n, w)) return rc;
+    } else {
+      if (int rc = ocp_global_jvp(ctx, jd, Q + (long long)jj * n, ctx->gm_t)) return rc;
+      if (int rc = ocp_ras_apply(ctx, fac, ctx->gm_t, w)) return rc;
+    }
     double* dh = ctx->gm_dh + (jj & 1) * hs;
     if (pipelined) {
       Timer t(ctx, CLS_MGS);
@@ -1063,6 +1168,20 @@ int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double re
   *resid_out = residual;
   *conv_out = converged ? 1 : 0;
   return OCP_OK;
+}
+
+int ocp_raspen_gmres(ocp_ctx* ctx, const double* fac, const double* b, double rel_tol,
+                     double abs_tol, int max_iters, double* x, int* iters_out, double* resid_out,
+                     int* conv_out, double* history) {
+  return gmres_impl(ctx, 0, fac, nullptr, b, rel_tol, abs_tol, max_iters, x, iters_out, resid_out,
+                    conv_out, history);
+}
+
+int ocp_ras_gmres(ocp_ctx* ctx, const double* jd, const double* fac, const double* b,
+                  double rel_tol, double abs_tol, int max_iters, double* x, int* iters_out,
+                  double* resid_out, int* conv_out, double* history) {
+  return gmres_impl(ctx, 1, fac, jd, b, rel_tol, abs_tol, max_iters, x, iters_out, resid_out,
+                    conv_out, history);
 }
 
 int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int k, const double* y_host,

@@ -72,14 +72,6 @@ __device__ __forceinline__ void stencil_point(const SubInfo& s, const Phys& P, c
   ap = add(slp, sep);
 }
 
-// residual rows (system.py:125-128)
-__device__ __forceinline__ void residual_rows(const Phys& P, double ay, double ap, double y, double p,
-                                              double f, double yd, double eps, double& r1, double& r2) {
-  const double ctrl = dvd(add(p, mul(P.mu, p_eps(dvd(-p, P.mu), eps))), P.nu);
-  r1 = add(sub(add(ay, phi_value(P, y)), f), ctrl);
-  r2 = add(sub(add(ap, mul(phi_d1(P, y), p)), y), yd);
-}
-
 // ---------------------------------------------------------------------------
 // gather v0 = x[pair_idx] into band order (schwarz.py:196)
 // ---------------------------------------------------------------------------

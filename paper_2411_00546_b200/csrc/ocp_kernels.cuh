@@ -33,6 +33,14 @@ __global__ void k_gemv_add(long long n, const double* Q, long long ldq, int k, c
                            const double* x, double* out);
 __global__ void k_recover_control(long long n, Phys P, const double* p, double eps, double* u);
 
+// whole-grid operators of newton-ras-eps (ocp_global.cu)
+__global__ void k_global_residual(Phys P, const double* x, const double* f, const double* yd,
+                                  double eps, double* r);
+__global__ void k_global_jacdiag(Phys P, const double* x, double eps, double4* JD,
+                                 unsigned long long* bad);
+__global__ void k_global_jvp(Phys P, const double4* JD, const double* d, double* out);
+__global__ void k_ras_out(const SubInfo* subs, Phys P, const double* Zpool, double* out);
+
 int factor_smem_bytes(int W);
 __global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
                               const double* JDpool, double* fac_pool, double* scratch,

@@ -286,8 +286,10 @@ class _RaspenOperator:
         self._check()
         return _jvp(self.engine, self.fac, d)
 
-    def fused_gmres(self, b, cfg):
+    def fused_gmres(self, b, cfg, precond=None):
         from .krylov import GmresBreakdownError, GmresResult
+        if precond is not None:
+            return NotImplemented
         self._check()
         e = self.engine
         x = e.vector(b.n)

@@ -9,6 +9,8 @@ Usage::
     python tests/golden/make_golden.py cfg1 [--inner-tol 1e-8] [--threads 8]
     python tests/golden/make_golden.py cfg5 --threads 8        # sweep + JVP
     python tests/golden/make_golden.py units                   # small unit fixtures
+    python tests/golden/make_golden.py ras_units               # linear-RAS operator fixtures
+    python tests/golden/make_golden.py ras_cfg1                # newton-ras-eps solve
 
 Settings are the harness-equivalent ones of SURVEY.md 0.10: outer tol 1e-10,
 GMRES rel 1e-8 / max 1000 (`harness/experiments.py:63-70`), inner tol as given
@@ -221,6 +223,99 @@ def run_units(out_path):
     np.savez_compressed(out_path, **data)
 
 
+def _ras_solve_args(spec, dec, gmres_tol=1e-8, tol=1e-10, sigma=1.1, max_outer=200):
+    """The `newton-ras-eps` branch of `solve_single` (`harness/experiments.py:72-84`)."""
+    from ocp.system import residual, jacobian
+
+    systems = ref_schwarz.build_local_systems(dec, spec)
+    newton_cfg = NewtonConfig(tol=tol, max_outer=max_outer, sigma=sigma,
+                              linear_solver=KrylovConfig(rel_tol=gmres_tol, max_iters=2000))
+    return (lambda x, eps: residual(x, spec, eps, check=False),
+            lambda x, eps: jacobian(x, spec, eps),
+            newton_cfg,
+            lambda x, eps: ref_schwarz.ras_preconditioner(x, dec, spec, eps, systems))
+
+
+def run_ras_units(out_path):
+    """Global residual / Jacobian action and one RAS preconditioner application
+    (`system.py:147-160`, `schwarz.py:221-239`), plus a small full solve."""
+    from ocp.newton import newton_continuation
+    from ocp.system import residual, jacobian
+    from paper_2411_00546_b200.problems import mild_spec
+
+    data = {}
+    cases = [
+        ("cubic20", 20, 2, 3, 2, make_phi("cubic"), 1e-3, 1e-2),
+        ("expm1_18", 18, 3, 2, 3, make_phi("expm1"), 1e-4, 5e-3),
+        ("kappa16", 16, 2, 2, 2, Nonlinearity(0.1), 1e-2, 1.0),
+    ]
+    for tag, n, s1, s2, m, phi, nu, mu in cases:
+        base = mild_spec(n)
+        grid = RefGrid(n)
+        spec = RefSpec(grid=grid, a=ref_laplacian(grid), phi=phi, nu=nu, mu=mu,
+                       f=base.f, y_d=10.0 * base.y_d)
+        dec = ref_schwarz.decompose(grid, s1, s2, m)
+        rng = np.random.default_rng(200 + n)
+        x = 0.3 * rng.standard_normal(2 * grid.size)
+        d = rng.standard_normal(2 * grid.size)
+        eps = 1e-2
+        data[f"{tag}_x"] = x
+        data[f"{tag}_d"] = d
+        data[f"{tag}_resid"] = residual(x, spec, eps, check=False)
+        data[f"{tag}_jvp"] = jacobian(x, spec, eps) @ d
+        data[f"{tag}_prec"] = ref_schwarz.ras_precondition(d, x, dec, spec, eps)
+        res_fn, jac_fn, ncfg, pb = _ras_solve_args(spec, dec)
+        xs, rep = newton_continuation(np.zeros_like(x), res_fn, jac_fn,
+                                      ContinuationSchedule(1.0, 0.2, 1e-3), ncfg,
+                                      precond_builder=pb)
+        data[f"{tag}_solve_x"] = xs
+        data[f"{tag}_solve_converged"] = rep.converged
+        data[f"{tag}_solve_outer"] = rep.outer_iters
+        data[f"{tag}_solve_gmres"] = np.array(rep.gmres_iters)
+        data[f"{tag}_solve_norms"] = np.array(rep.residual_norms)
+        data[f"{tag}_solve_alphas"] = np.array(rep.alphas)
+        print(f"{tag}: ras solve outer={rep.outer_iters} gmres={rep.gmres_iters} "
+              f"alphas={rep.alphas} conv={rep.converged}")
+    np.savez_compressed(out_path, **data)
+
+
+def run_ras_solve(name, out_path):
+    """`newton-ras-eps` on a BASELINE configuration (harness settings)."""
+    from ocp.newton import newton_continuation
+
+    cfg = CONFIGS[name]
+    spec = ref_spec(cfg)
+    dec = ref_schwarz.decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    sched = ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)
+    res_fn, jac_fn, ncfg, pb = _ras_solve_args(spec, dec)
+    t0 = time.perf_counter()
+    x, report = newton_continuation(np.zeros(2 * spec.grid.size), res_fn, jac_fn, sched, ncfg,
+                                    precond_builder=pb)
+    wall = time.perf_counter() - t0
+    n2 = spec.grid.size
+    y, p = x[:n2], x[n2:]
+    u = recover_control(p, spec, cfg.eps_min)
+    data = dict(
+        config=name, method="newton-ras-eps", wall=wall,
+        converged=report.converged, outer_iters=report.outer_iters,
+        residual_norms=np.array(report.residual_norms),
+        eps_values=np.array(report.eps_values),
+        alphas=np.array(report.alphas),
+        gmres_iters=np.array([-1 if k is None else k for k in report.gmres_iters]),
+        threshold=report.threshold,
+        failure="" if report.failure is None else report.failure,
+    )
+    if n2 <= 256 * 256:
+        data.update(y=y, p=p, u=u)
+    for key, vec in (("y", y), ("p", p), ("u", u)):
+        for k, v in digest(vec).items():
+            data[f"{key}_{k}"] = v
+    np.savez_compressed(out_path, **data)
+    print(f"ras {name}: converged={report.converged} outer={report.outer_iters} "
+          f"gmres={report.gmres_iters} alphas={report.alphas} failure={report.failure} "
+          f"wall={wall:.1f}s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("what")
@@ -230,6 +325,10 @@ def main():
     args = ap.parse_args()
     if args.what == "units":
         run_units(args.out or os.path.join(HERE, "units.npz"))
+    elif args.what == "ras_units":
+        run_ras_units(args.out or os.path.join(HERE, "ras_units.npz"))
+    elif args.what.startswith("ras_cfg"):
+        run_ras_solve(args.what[4:], args.out or os.path.join(HERE, f"{args.what}.npz"))
     elif args.what.startswith("cfg5"):
         run_sweep(args.what, args.threads, args.out or os.path.join(HERE, f"{args.what}_sweep.npz"))
     else:

@@ -104,3 +104,44 @@ def test_golden_records_are_consistent():
             np.testing.assert_array_equal(g["per_sub"].max(axis=1), g["inner_iters"])
         else:
             assert "subdomain" in str(g["failure"]), path
+
+
+# ---------------------------------------------------------------------------
+# linear-RAS Newton-Krylov (newton-ras-eps): global residual / Jacobian, the
+# RAS preconditioner and full solves, fixtures from the unmodified reference
+# (make_golden.py ras_units / ras_cfg1 / ras_cfg2)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", UNIT_CASES, ids=[c[0] for c in UNIT_CASES])
+def test_oracle_ras_units_bitwise(case):
+    tag, n, s1, s2, m, phi, nu, mu = case
+    g = golden("ras_units.npz")
+    prob = unit_problem(n, s1, s2, m, phi, nu, mu)
+    x, d, eps = g[f"{tag}_x"], g[f"{tag}_d"], 1e-2
+    np.testing.assert_array_equal(O.global_residual(prob, x, eps), g[f"{tag}_resid"])
+    np.testing.assert_array_equal(O.global_jacobian(prob, x, eps) @ d, g[f"{tag}_jvp"])
+    np.testing.assert_array_equal(O.ras_preconditioner(prob, x, eps)(d), g[f"{tag}_prec"])
+    with threadpool_limits(1, "blas"):
+        xs, rep = O.newton_ras_solve(prob, np.zeros_like(x), 1.0, 0.2, 1e-3)
+    np.testing.assert_array_equal(xs, g[f"{tag}_solve_x"])
+    assert rep["outer_iters"] == int(g[f"{tag}_solve_outer"])
+    assert rep["gmres_iters"] == list(g[f"{tag}_solve_gmres"])
+    assert rep["alphas"] == list(g[f"{tag}_solve_alphas"])
+    np.testing.assert_array_equal(rep["residual_norms"], g[f"{tag}_solve_norms"])
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_oracle_ras_cfg_bitwise(name):
+    g = golden(f"ras_{name}.npz")
+    cfg, prob = _cfg_problem(name)
+    with threadpool_limits(1, "blas"):
+        x, rep = O.newton_ras_solve(prob, np.zeros(2 * cfg.n * cfg.n), cfg.eps0, cfg.gamma,
+                                    cfg.eps_min)
+    assert rep["converged"] == bool(g["converged"])
+    assert rep["outer_iters"] == int(g["outer_iters"])
+    assert rep["gmres_iters"] == list(g["gmres_iters"])
+    assert rep["alphas"] == list(g["alphas"])
+    np.testing.assert_array_equal(rep["residual_norms"], g["residual_norms"])
+    n2 = cfg.n * cfg.n
+    np.testing.assert_array_equal(x[:n2], g["y"])
+    np.testing.assert_array_equal(x[n2:], g["p"])
