@@ -48,7 +48,8 @@ enum { OCP_PHI_KAPPA = 0, OCP_PHI_CUBIC = 1, OCP_PHI_EXPM1 = 2 };
  * Replaces decompose + build_local_systems (schwarz.py:94-163): builds the
  * reference tiling (_tile_edges: remainder to the last tile, overlap clipped),
  * uploads f and y_d, sizes the local pools.  Errors mirror decompose's
- * ValueErrors (message in ocp_last_error(NULL) when *out is not created). */
+ * ValueErrors (message in ocp_last_error(NULL) when *out is not created).
+ * s1 = s2 = 0 creates a grid-only context (whole-grid operators, no subdomains). */
 int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu,
                    int phi_kind, double kappa, const double* f_host,
                    const double* y_d_host, ocp_ctx** out);
@@ -174,6 +175,23 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac_dev, const double* v_dev, doub
 int ocp_ras_gmres(ocp_ctx* ctx, const double* jd_dev, const double* fac_dev, const double* b_dev,
                   double rel_tol, double abs_tol, int max_iters, double* x_dev, int* iters_host,
                   double* residual_host, int* converged_host, double* history_host);
+
+/* ---- manufactured-problem setup on the device (system.py:181-265) -------
+ * A context created with s1 = s2 = 0 is grid-only (no subdomains): the
+ * whole-grid and state-equation entry points work, the subdomain ones
+ * return OCP_ERR_ARG. */
+/* out = A y + phi(y) - rhs  (solve_state's residual, check=False, system.py:188-189) */
+int ocp_state_residual(ocp_ctx* ctx, const double* y_dev, const double* rhs_dev, double* out_dev);
+/* (A + diag(phi'(y))) x = b by CG from x = 0 to ||r|| <= rel_tol ||b||: the
+ * device replacement of the direction solve splu(state_jacobian(y)).solve
+ * (system.py:191-196); OCP_ERR_NONFINITE "phi'(y)@k" like the reference's
+ * derivative check.  *converged_host = 0 when max_iters is reached. */
+int ocp_state_cg(ocp_ctx* ctx, const double* y_dev, const double* b_dev, double rel_tol,
+                 int max_iters, double* x_dev, int* iters_host, double* residual_host,
+                 int* converged_host);
+/* y_d = y_bar - A p_bar - phi'(y_bar) p_bar  (_manufacture, system.py:263) */
+int ocp_manufacture_yd(ocp_ctx* ctx, const double* ybar_dev, const double* pbar_dev,
+                       double* yd_dev);
 
 /* u = -(p + mu P_eps(-p/mu))/nu  (system.py:173-174) */
 int ocp_recover_control(ocp_ctx* ctx, long long n, const double* p, double eps,

@@ -22,3 +22,6 @@ from .engine import DeviceVector, Engine
 from ._native import NativeError, NativeUnavailable
 from .linear_ras import (GlobalJacobian, RasPreconditioner, global_jacobian, global_residual,
                          newton_ras_solve, ras_precondition, ras_preconditioner)
+from .problem_setup import (StatePair, construct_plateau_problem, construct_test_problem,
+                            solve_state)
+from . import harness

@@ -45,6 +45,7 @@ def build(force=False, verbose=False):
     if not force and not stale():
         return LIB
     extra = ["-DOCP_PHASE_TIMING"] if os.environ.get("OCP_PHASE_TIMING") else []
+    extra += os.environ.get("OCP_EXTRA_NVCC", "").split()   # experiments only
     cmd = [nvcc()] + NVCC_FLAGS + extra + ["-o", LIB] + sources()
     if verbose:
         print(" ".join(cmd), flush=True)

@@ -66,6 +66,9 @@ SIGNATURES = {
     "ocp_ras_factor": [_vp, _vp, _d, _vp, _c_int_p],
     "ocp_ras_apply": [_vp, _vp, _vp, _vp],
     "ocp_ras_gmres": [_vp, _vp, _vp, _vp, _d, _d, _i, _vp, _c_int_p, _c_dbl_p, _c_int_p, _c_dbl_p],
+    "ocp_state_residual": [_vp, _vp, _vp, _vp],
+    "ocp_state_cg": [_vp, _vp, _vp, _d, _i, _vp, _c_int_p, _c_dbl_p, _c_int_p],
+    "ocp_manufacture_yd": [_vp, _vp, _vp, _vp],
     "ocp_gemv_add": [_vp, _ll, _vp, _ll, _i, _c_dbl_p, _vp, _vp],
     "ocp_recover_control": [_vp, _ll, _vp, _d, _vp],
     "ocp_set_profiling": [_vp, _i],

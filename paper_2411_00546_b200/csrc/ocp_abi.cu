@@ -70,6 +70,11 @@ struct ocp_ctx {
   int gm_hcap = 0;             // entries per slot
   cudaEvent_t gm_ev[2] = {nullptr, nullptr};
   double* gm_t = nullptr;      // J q_j of the preconditioned (linear-RAS) operator
+  double* st_buf = nullptr;    // state-equation CG: dg, r, p, Ap (4 N doubles)
+  double* st_sc = nullptr;     // CG scalars (rr, pAp, alpha, beta)
+  double* st_hist = nullptr;   // CG r.r history (device) ...
+  double* st_hhist = nullptr;  // ... and its pinned host copy
+  int st_hcap = 0;
   unsigned long long* d_gbad = nullptr;   // first nonfinite phi'/phi'' of the global Jacobian
   int h_cap = 0;
   cudaStream_t stream = nullptr;
@@ -263,15 +268,20 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   if (!out) return fail(nullptr, OCP_ERR_ARG, "null output pointer");
   *out = nullptr;
   if (n < 1) return fail(nullptr, OCP_ERR_ARG, "grid needs at least one interior point per dimension");
-  if (s1 < 1 || s2 < 1) return fail(nullptr, OCP_ERR_ARG, "need at least one tile per dimension");
+  const bool grid_only = (s1 == 0 && s2 == 0);   // whole-grid operators only, no subdomains
+  if (!grid_only && (s1 < 1 || s2 < 1))
+    return fail(nullptr, OCP_ERR_ARG, "need at least one tile per dimension");
   if (overlap < 0) return fail(nullptr, OCP_ERR_ARG, "overlap must be nonnegative");
   if (!(nu > 0.0) || !(mu > 0.0)) return fail(nullptr, OCP_ERR_ARG, "nu and mu must be positive");
   if (phi_kind < 0 || phi_kind > 2) return fail(nullptr, OCP_ERR_ARG, "unknown phi kind %d", phi_kind);
-  bool ok1, ok2;
-  auto rt = tile_edges(n, s1, ok1);
-  if (!ok1) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s1);
-  auto ct = tile_edges(n, s2, ok2);
-  if (!ok2) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s2);
+  bool ok1 = true, ok2 = true;
+  std::vector<std::pair<int, int>> rt, ct;
+  if (!grid_only) {
+    rt = tile_edges(n, s1, ok1);
+    if (!ok1) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s1);
+    ct = tile_edges(n, s2, ok2);
+    if (!ok2) return fail(nullptr, OCP_ERR_ARG, "cannot tile %d points into %d nonempty parts", n, s2);
+  }
   auto minw = [](const std::vector<std::pair<int, int>>& t) {
     int m = INT_MAX;
     for (auto& e : t) m = std::min(m, e.second - e.first);
@@ -459,12 +469,13 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
+                  (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
                   (void*)ctx->d_gbad,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
                   (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
-                  (void*)ctx->gm_hh})
+                  (void*)ctx->gm_hh, (void*)ctx->st_hhist})
     if (p) cudaFreeHost(p);
   for (auto e : ctx->gm_ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pending) {
@@ -545,6 +556,7 @@ int ocp_sync(ocp_ctx* ctx) {
 int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0, double gamma,
                         double eps_min, double tol, int max_outer, double sigma, int max_halvings,
                         double* fval, int* inner_iters, int* failed_sub) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   if (!ctx || !x || !fac || !fval) return fail(ctx, OCP_ERR_ARG, "null argument");
   const int I = ctx->I;
   cudaStream_t st = ctx->stream;
@@ -707,6 +719,7 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
 }
 
 int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   if (!ctx || !fac || !d || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
@@ -728,12 +741,14 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
 }
 
 int ocp_local_values(ocp_ctx* ctx, double* values) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   k_band_to_ref<<<ctx->I, 256, 0, ctx->stream>>>(ctx->d_subs, ctx->V, values);
   CKL();
   return OCP_OK;
 }
 
 int ocp_local_residual(ocp_ctx* ctx, const double* x, const double* v_ref, double eps, double* r_ref) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
   k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
@@ -746,6 +761,7 @@ int ocp_local_residual(ocp_ctx* ctx, const double* x, const double* v_ref, doubl
 }
 
 int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, double eps, double* d_ref) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
   double* fac = nullptr;
@@ -943,6 +959,7 @@ int ocp_global_jvp(ocp_ctx* ctx, const double* jd, const double* d, double* out)
 // local Jacobians at x restricted to every subdomain, factored into fac
 // (ras_preconditioner, schwarz.py:221-232)
 int ocp_ras_factor(ocp_ctx* ctx, const double* x, double eps, double* fac, int* failed_sub) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   if (!ctx || !x || !fac) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
@@ -975,6 +992,7 @@ int ocp_ras_factor(ocp_ctx* ctx, const double* x, double eps, double* fac, int* 
 
 // out = sum_i P~_i J_i^{-1} R_i v  (the apply closure, schwarz.py:234-239)
 int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   if (!ctx || !fac || !v || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
@@ -990,6 +1008,93 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out)
   }
   k_ras_out<<<dim3(I, 4), 256, 0, st>>>(ctx->d_subs, ctx->P, ctx->B, out);
   CKL();
+  return OCP_OK;
+}
+
+// ---- state equation of the manufactured problems (system.py:181-197) ----
+int ocp_state_residual(ocp_ctx* ctx, const double* y, const double* rhs, double* out) {
+  if (!ctx || !y || !rhs || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
+  k_state_residual<<<ew_grid(ctx->N), 256, 0, ctx->stream>>>(ctx->P, y, rhs, out);
+  CKL();
+  return OCP_OK;
+}
+
+int ocp_manufacture_yd(ocp_ctx* ctx, const double* ybar, const double* pbar, double* yd) {
+  if (!ctx || !ybar || !pbar || !yd) return fail(ctx, OCP_ERR_ARG, "null argument");
+  k_manufacture_yd<<<ew_grid(ctx->N), 256, 0, ctx->stream>>>(ctx->P, ybar, pbar, yd);
+  CKL();
+  CK(cudaStreamSynchronize(ctx->stream));
+  return OCP_OK;
+}
+
+// (A + diag(phi'(y))) x = b by conjugate gradients from x = 0 until
+// ||r|| <= rel_tol ||b|| (the matrix is SPD for the phi families used:
+// phi' >= 0).  Scalars stay on the device; the host polls the r.r history
+// every CG_POLL iterations (the few extra iterations only tighten x).
+int ocp_state_cg(ocp_ctx* ctx, const double* y, const double* b, double rel_tol, int max_iters,
+                 double* x, int* iters_out, double* resid_out, int* conv_out) {
+  if (!ctx || !y || !b || !x || max_iters < 1) return fail(ctx, OCP_ERR_ARG, "bad argument");
+  constexpr int CG_POLL = 16;
+  cudaStream_t st = ctx->stream;
+  const long long N = ctx->N;
+  if (!ctx->st_buf) {
+    CK(cudaMalloc(&ctx->st_buf, 4 * (size_t)N * sizeof(double)));
+    CK(cudaMalloc(&ctx->st_sc, 8 * sizeof(double)));
+  }
+  const int hcap = max_iters + CG_POLL;
+  if (ctx->st_hcap < hcap) {
+    cudaStreamSynchronize(st);
+    if (ctx->st_hist) cudaFree(ctx->st_hist);
+    if (ctx->st_hhist) cudaFreeHost(ctx->st_hhist);
+    CK(cudaMalloc(&ctx->st_hist, hcap * sizeof(double)));
+    CK(cudaMallocHost(&ctx->st_hhist, hcap * sizeof(double)));
+    ctx->st_hcap = hcap;
+  }
+  if (!ctx->d_gbad) CK(cudaMalloc(&ctx->d_gbad, sizeof(unsigned long long)));
+  double *dg = ctx->st_buf, *r = dg + N, *p = r + N, *Ap = p + N;
+  CK(cudaMemsetAsync(ctx->d_gbad, 0xff, sizeof(unsigned long long), st));
+  k_state_diag<<<ew_grid(N), 256, 0, st>>>(ctx->P, y, dg, ctx->d_gbad);
+  CKL();
+  CK(cudaMemsetAsync(x, 0, N * sizeof(double), st));
+  CK(cudaMemcpyAsync(r, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(p, b, N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  k_dot<<<RED_BLOCKS, RED_THREADS, 0, st>>>(N, b, b, ctx->red_partials, ctx->red_counter,
+                                            ctx->st_sc, 0);
+  CKL();
+  unsigned long long bad = 0;
+  double bb = 0.0;
+  CK(cudaMemcpyAsync(&bad, ctx->d_gbad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&bb, ctx->st_sc, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (bad != ~0ull) return fail(ctx, OCP_ERR_NONFINITE, "phi'(y)@%lld", (long long)bad);
+  const double thr2 = rel_tol * rel_tol * bb;
+  *iters_out = 0; *resid_out = std::sqrt(bb); *conv_out = 1;
+  if (bb == 0.0) return OCP_OK;
+  int it = 0;
+  while (it < max_iters) {
+    const int it0 = it;
+    for (int q = 0; q < CG_POLL && it < max_iters; ++q, ++it) {
+      k_cg_ap<<<RED_BLOCKS, RED_THREADS, 0, st>>>(ctx->P, dg, p, Ap, ctx->red_partials,
+                                                  ctx->red_counter, ctx->st_sc);
+      k_cg_xr<<<RED_BLOCKS, RED_THREADS, 0, st>>>(N, p, Ap, x, r, ctx->red_partials,
+                                                  ctx->red_counter, ctx->st_sc, ctx->st_hist, it);
+      k_cg_p<<<ew_grid(N), 256, 0, st>>>(N, r, p, ctx->st_sc);
+      ctx->launches += 3;
+    }
+    CKL();
+    CK(cudaMemcpyAsync(ctx->st_hhist + it0, ctx->st_hist + it0, (it - it0) * sizeof(double),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int k = it0; k < it; ++k) {
+      const double rr = ctx->st_hhist[k];
+      if (!std::isfinite(rr)) return fail(ctx, OCP_ERR_NONFINITE, "CG residual@%d", k);
+      if (rr <= thr2) {
+        *iters_out = it; *resid_out = std::sqrt(ctx->st_hhist[it - 1]);
+        return OCP_OK;
+      }
+    }
+  }
+  *iters_out = it; *resid_out = std::sqrt(ctx->st_hhist[it - 1]); *conv_out = 0;
   return OCP_OK;
 }
 

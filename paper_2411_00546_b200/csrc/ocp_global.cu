@@ -5,6 +5,10 @@
 //   k_global_jacdiag   Jacobian diagonals + finite checks  system.py:135-144,155-160
 //   k_global_jvp       J(x) d, the CSR row sums of bmat    system.py:155-160
 //   k_ras_out          out[own_i] = z_i[own_in_local]       schwarz.py:234-239
+//   k_state_*          the semilinear state equation A y + phi(y) = f + u of
+//                      the manufactured problems (system.py:181-197, 257-265):
+//                      residual, diagonal of A + diag(phi'(y)), matrix-free CG
+//                      steps with device-side scalars, and y_d of _manufacture
 //
 // Every row sum follows the reference's CSR entry order (columns ascending,
 // scipy csr_matvec: sum starts at 0.0, one rounded product and one rounded
@@ -12,6 +16,7 @@
 // finite inputs.  Threads run along the global column index: all loads are
 // coalesced, the +-1 / +-n neighbours hit L1/L2.
 #include "ocp_kernels.cuh"
+#include "ocp_reduce.cuh"
 
 namespace ocp {
 
@@ -106,6 +111,132 @@ __global__ void k_ras_out(const SubInfo* subs, Phys P, const double* Zpool, doub
     const double2 z = Z[global_to_q(s, i, j)];
     out[g] = z.x;
     out[Ntot + g] = z.y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// state equation (solve_state, system.py:181-197)
+// ---------------------------------------------------------------------------
+// (A v)[k] in the kron Laplacian's CSR order with diagonal entry dk
+__device__ __forceinline__ double stencil_row(const Phys& P, const double* v, long long k, int i, int j,
+                                              double dk) {
+  const int n = P.n;
+  double s = 0.0;
+  if (i > 0) s = add(s, mul(P.off, v[k - n]));
+  if (j > 0) s = add(s, mul(P.off, v[k - 1]));
+  s = add(s, mul(dk, v[k]));
+  if (j < n - 1) s = add(s, mul(P.off, v[k + 1]));
+  if (i < n - 1) s = add(s, mul(P.off, v[k + n]));
+  return s;
+}
+
+// out = A y + phi(y) - rhs   (state_residual, check=False, system.py:188-189)
+__global__ void __launch_bounds__(256) k_state_residual(Phys P, const double* __restrict__ y,
+                                                        const double* __restrict__ rhs,
+                                                        double* __restrict__ out) {
+  const int n = P.n;
+  const long long N = (long long)n * n;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(k / n), j = (int)(k - (long long)i * n);
+    out[k] = sub(add(stencil_row(P, y, k, i, j, P.diag), phi_value(P, y[k])), rhs[k]);
+  }
+}
+
+// dg[k] = 4/h^2 + phi'(y_k): the diagonal of (A + diags(phi'(y))).tocsr()
+// (state_jacobian, system.py:191-192; phi.derivative checks => *bad)
+__global__ void __launch_bounds__(256) k_state_diag(Phys P, const double* __restrict__ y,
+                                                    double* __restrict__ dg,
+                                                    unsigned long long* bad) {
+  const long long N = (long long)P.n * P.n;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x) {
+    const double d1 = phi_d1(P, y[k]);
+    bool b = !isfinite(d1);
+    if (P.phi_kind == 0 && P.kappa != 0.0 && mul(P.kappa, y[k]) > 700.0) b = true;
+    if (P.phi_kind == 2 && y[k] > 700.0) b = true;
+    if (b) atomicMin(bad, (unsigned long long)k);
+    dg[k] = add(P.diag, d1);
+  }
+}
+
+// CG scalars on the device: sc[0] = r.r, sc[1] = p.Ap, sc[2] = alpha,
+// sc[3] = beta; hist[it] = r.r after iteration it
+__global__ void __launch_bounds__(RED_THREADS) k_cg_ap(Phys P, const double* __restrict__ dg,
+                                                       const double* __restrict__ p,
+                                                       double* __restrict__ Ap, double* partials,
+                                                       unsigned int* counter, double* sc) {
+  __shared__ double red[32];
+  const int n = P.n;
+  const long long N = (long long)n * n;
+  double acc = 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(k / n), j = (int)(k - (long long)i * n);
+    const double v = stencil_row(P, p, k, i, j, dg[k]);
+    Ap[k] = v;
+    acc = fma(p[k], v, acc);
+  }
+  const double tot = block_sum<RED_THREADS>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  if (!last_block_done(counter)) return;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += partials[b];
+  const double pap = block_sum<RED_THREADS>(v, red);
+  if (threadIdx.x == 0) {
+    sc[1] = pap;
+    sc[2] = sc[0] / pap;
+    *counter = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(RED_THREADS) k_cg_xr(long long N, const double* __restrict__ p,
+                                                       const double* __restrict__ Ap,
+                                                       double* __restrict__ x, double* __restrict__ r,
+                                                       double* partials, unsigned int* counter,
+                                                       double* sc, double* hist, int it) {
+  __shared__ double red[32];
+  const double alpha = sc[2];
+  double acc = 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x) {
+    x[k] = fma(alpha, p[k], x[k]);
+    const double rk = fma(-alpha, Ap[k], r[k]);
+    r[k] = rk;
+    acc = fma(rk, rk, acc);
+  }
+  const double tot = block_sum<RED_THREADS>(acc, red);
+  if (threadIdx.x == 0) partials[blockIdx.x] = tot;
+  if (!last_block_done(counter)) return;
+  double v = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) v += partials[b];
+  const double rr = block_sum<RED_THREADS>(v, red);
+  if (threadIdx.x == 0) {
+    sc[3] = rr / sc[0];
+    sc[0] = rr;
+    hist[it] = rr;
+    *counter = 0u;
+  }
+}
+
+__global__ void k_cg_p(long long N, const double* __restrict__ r, double* __restrict__ p,
+                       const double* sc) {
+  const double beta = sc[3];
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x)
+    p[k] = fma(beta, p[k], r[k]);
+}
+
+// y_d = y_bar - A p_bar - phi'(y_bar) p_bar   (_manufacture, system.py:263)
+__global__ void __launch_bounds__(256) k_manufacture_yd(Phys P, const double* __restrict__ ybar,
+                                                        const double* __restrict__ pbar,
+                                                        double* __restrict__ yd) {
+  const int n = P.n;
+  const long long N = (long long)n * n;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+       k += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(k / n), j = (int)(k - (long long)i * n);
+    yd[k] = sub(sub(ybar[k], stencil_row(P, pbar, k, i, j, P.diag)), mul(phi_d1(P, ybar[k]), pbar[k]));
   }
 }
 

@@ -5,29 +5,13 @@
 // (system.py:118-144, schwarz.py:174-186, scipy CSR row order), so the local
 // residuals match the CPU oracle bitwise for the polynomial phi's.
 #include "ocp_kernels.cuh"
+#include "ocp_reduce.cuh"
 
 namespace ocp {
 
 // ---------------------------------------------------------------------------
 // deterministic block reduction (fixed tree, fixed blockDim)
 // ---------------------------------------------------------------------------
-template <int THREADS>
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (wid == 0) {
-    r = lane < THREADS / 32 ? red[lane] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-  }
-  __syncthreads();
-  return r;  // valid in thread 0
-}
-
 // ---------------------------------------------------------------------------
 // local value of the (optionally line-searched) iterate: v + alpha*d
 // (newton.py:106: x + alpha * d, product rounded first)
@@ -419,18 +403,6 @@ __global__ void k_band_to_ref(const SubInfo* subs, const double* pool, double* r
 // "last block reduces" pattern: partials in fixed slots, the last block to
 // finish sums them in a fixed tree.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool last_block_done(unsigned int* counter) {
-  __shared__ bool is_last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int ticket = atomicAdd(counter, 1u);
-    is_last = (ticket == gridDim.x - 1);
-  }
-  __syncthreads();
-  return is_last;
-}
-
 __device__ __forceinline__ void finish_reduction(double* partials, unsigned int* counter,
                                                  double* result, bool take_sqrt, double* red) {
   if (!last_block_done(counter)) return;

@@ -40,6 +40,14 @@ __global__ void k_global_jacdiag(Phys P, const double* x, double eps, double4* J
                                  unsigned long long* bad);
 __global__ void k_global_jvp(Phys P, const double4* JD, const double* d, double* out);
 __global__ void k_ras_out(const SubInfo* subs, Phys P, const double* Zpool, double* out);
+__global__ void k_state_residual(Phys P, const double* y, const double* rhs, double* out);
+__global__ void k_state_diag(Phys P, const double* y, double* dg, unsigned long long* bad);
+__global__ void k_cg_ap(Phys P, const double* dg, const double* p, double* Ap, double* partials,
+                        unsigned int* counter, double* sc);
+__global__ void k_cg_xr(long long N, const double* p, const double* Ap, double* x, double* r,
+                        double* partials, unsigned int* counter, double* sc, double* hist, int it);
+__global__ void k_cg_p(long long N, const double* r, double* p, const double* sc);
+__global__ void k_manufacture_yd(Phys P, const double* ybar, const double* pbar, double* yd);
 
 int factor_smem_bytes(int W);
 __global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,

@@ -61,7 +61,8 @@ class GlobalJacobian:
 
     def __init__(self, engine, x, eps):
         xd, _ = _as_device(engine, x)
-        self.engine, self.eps = engine, float(eps)
+        self.engine, self.eps, self.x = engine, float(eps), xd
+        self._lu = None
         self.jd = engine.buffer(8 * 4 * engine.N)
         rc = engine.lib.ocp_global_jacobian(engine.ctx, xd.ptr, self.eps,
                                             ctypes.c_void_p(self.jd.addr))
@@ -76,6 +77,16 @@ class GlobalJacobian:
         return out if dev else out.to_host()
 
     __matmul__ = __call__
+
+    def direct_solve(self, rhs):
+        """Sparse direct solve of J d = rhs (splu, `newton.py:125-129`): the
+        batched banded LU on a single-subdomain engine, i.e. one LU of the
+        whole Jacobian (half-bandwidth 2n: grids up to n = 112)."""
+        if self.engine.num_subdomains != 1:
+            raise ValueError("direct solves need the single-subdomain (1x1) engine")
+        if self._lu is None:
+            self._lu = RasPreconditioner(self.engine, self.x, self.eps)
+        return self._lu(rhs)
 
     def fused_gmres(self, b, cfg, precond=None):
         """Whole preconditioned GMRES solve natively when ``precond`` is this

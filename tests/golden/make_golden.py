@@ -316,6 +316,47 @@ def run_ras_solve(name, out_path):
           f"wall={wall:.1f}s")
 
 
+HARNESS_CASES = [
+    ("newton_eps", dict(method="newton-eps")),
+    ("newton", dict(method="newton", eps0=1e-3)),
+    ("newton_eps_gmres", dict(method="newton-eps", linear_solver="gmres")),
+    ("newton_ras_eps", dict(method="newton-ras-eps", s1=2, s2=2, overlap=2)),
+    ("raspen_eps", dict(method="raspen-eps", s1=2, s2=2, overlap=2)),
+    ("raspen_eps_23", dict(method="raspen-eps", n=20, s1=2, s2=3, overlap=1, k_tilde=3)),
+    ("fail_max_outer", dict(method="newton-eps", max_outer=1, eps_min=1e-10)),
+]
+HARNESS_MILD = dict(n=12, nu=1e-2, k_tilde=2, eps_min=1e-3)   # pkg/tests/test_harness.py:27
+
+
+def run_harness(out_path):
+    """Artifacts of the reference's run_single (`harness/experiments.py:102-117`)
+    on the mild configuration family of its own tests, plus manufactured
+    problems (`system.py:219-265`)."""
+    import tempfile
+    from pathlib import Path
+    from ocp.harness.config import build_config
+    from ocp.harness.experiments import run_single
+    from ocp.system import construct_plateau_problem, construct_test_problem
+
+    data = {}
+    for tag, over in HARNESS_CASES:
+        cfg = build_config(overrides={**HARNESS_MILD, **over})
+        with tempfile.TemporaryDirectory() as tmp:
+            code, rep = run_single(cfg, tmp)
+            for name in ("report.json", "residual_history.csv", "y.csv", "p.csv", "u.csv"):
+                data[f"{tag}__{name}"] = np.array((Path(tmp) / name).read_text())
+        data[f"{tag}__code"] = code
+        print(f"harness {tag}: code={code} outer={rep['outer_iters']} gmres={rep['gmres_iters']}")
+    for tag, n, kw in (("test12", 12, dict(kappa=0.1, nu=1e-2, mu=1.0, k_tilde=2)),
+                       ("test40", 40, dict(kappa=0.1, nu=1e-6, mu=1.0, k_tilde=5))):
+        spec, pair = construct_test_problem(RefGrid(n), **kw)
+        data[f"mfg_{tag}_yd"], data[f"mfg_{tag}_y"], data[f"mfg_{tag}_p"] = spec.y_d, pair.y, pair.p
+    spec, pair = construct_plateau_problem(RefGrid(24), kappa=0.1, nu=1e-3, mu=1.0)
+    data["mfg_plateau24_yd"], data["mfg_plateau24_y"], data["mfg_plateau24_p"] = \
+        spec.y_d, pair.y, pair.p
+    np.savez_compressed(out_path, **data)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("what")
@@ -325,6 +366,8 @@ def main():
     args = ap.parse_args()
     if args.what == "units":
         run_units(args.out or os.path.join(HERE, "units.npz"))
+    elif args.what == "harness":
+        run_harness(args.out or os.path.join(HERE, "harness.npz"))
     elif args.what == "ras_units":
         run_ras_units(args.out or os.path.join(HERE, "ras_units.npz"))
     elif args.what.startswith("ras_cfg"):

@@ -1,0 +1,114 @@
+"""GPU runs of the orchestration layer against the reference's own artifacts.
+
+Fixtures: ``tests/golden/harness.npz`` (reference ``run_single`` on the mild
+configuration family of `pkg/tests/test_harness.py:27`, and manufactured
+problems of `system.py:219-265`).
+
+Bar: exit code, outer iterations, step lengths and eps history identical;
+GMRES iterations within +-1 per step; y/p/u within 1e-8 relative L2; residual
+history within 1e-8 relative above the solver's noise floor; a second run
+reproduces every artifact byte for byte apart from timing (`test_harness.py:167-176`).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from paper_2411_00546_b200.grid import Grid
+from paper_2411_00546_b200.harness import ExperimentConfig, read_field_csv, run_single
+from paper_2411_00546_b200.problem_setup import (construct_plateau_problem,
+                                                 construct_test_problem, solve_state)
+
+pytestmark = pytest.mark.gpu
+
+MILD = dict(n=12, nu=1e-2, k_tilde=2, eps_min=1e-3)
+CASES = {
+    "newton_eps": dict(method="newton-eps"),
+    "newton": dict(method="newton", eps0=1e-3),
+    "newton_eps_gmres": dict(method="newton-eps", linear_solver="gmres"),
+    "newton_ras_eps": dict(method="newton-ras-eps", s1=2, s2=2, overlap=2),
+    "raspen_eps": dict(method="raspen-eps", s1=2, s2=2, overlap=2),
+    "raspen_eps_23": dict(method="raspen-eps", n=20, s1=2, s2=3, overlap=1, k_tilde=3),
+    "fail_max_outer": dict(method="newton-eps", max_outer=1, eps_min=1e-10),
+}
+
+
+def rel_l2(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _native(native_gpu):
+    return native_gpu
+
+
+@pytest.mark.parametrize("tag,n,kw", [
+    ("test12", 12, dict(kappa=0.1, nu=1e-2, mu=1.0, k_tilde=2)),
+    ("test40", 40, dict(kappa=0.1, nu=1e-6, mu=1.0, k_tilde=5)),
+])
+def test_manufactured_problem_on_device(tag, n, kw):
+    g = golden("harness.npz")
+    spec, pair = construct_test_problem(Grid(n), **kw)
+    np.testing.assert_array_equal(pair.p, g[f"mfg_{tag}_p"])
+    assert rel_l2(pair.y, g[f"mfg_{tag}_y"]) <= 1e-12
+    assert rel_l2(spec.y_d, g[f"mfg_{tag}_yd"]) <= 1e-12
+
+
+def test_plateau_problem_on_device():
+    g = golden("harness.npz")
+    spec, pair = construct_plateau_problem(Grid(24), kappa=0.1, nu=1e-3, mu=1.0)
+    np.testing.assert_array_equal(pair.p, g["mfg_plateau24_p"])
+    assert rel_l2(pair.y, g["mfg_plateau24_y"]) <= 1e-12
+    assert rel_l2(spec.y_d, g["mfg_plateau24_yd"]) <= 1e-12
+
+
+def test_solve_state_residual_small():
+    spec, pair = construct_test_problem(Grid(32), kappa=0.1, nu=1e-2, mu=1.0, k_tilde=2)
+    u = np.sin(np.arange(32 * 32) * 0.1)
+    y = solve_state(u, spec)
+    from paper_2411_00546_b200.grid import build_laplacian
+    a = build_laplacian(spec.grid)
+    r = a @ y + spec.phi.value(y) - (spec.f + u)
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(spec.f + u)
+
+
+@pytest.mark.parametrize("tag", list(CASES))
+def test_run_single_matches_reference_artifacts(tag, tmp_path):
+    g = golden("harness.npz")
+    ref = json.loads(str(g[f"{tag}__report.json"]))
+    cfg = ExperimentConfig(**{**MILD, **CASES[tag]})
+    code, data = run_single(cfg, tmp_path)
+    assert code == int(g[f"{tag}__code"])
+    assert data["config"] == ref["config"]
+    for key in ("converged", "outer_iters", "alphas", "eps_history", "inner_iters"):
+        assert data[key] == ref[key], key
+    assert (data["failure"] is None) == (ref["failure"] is None)
+    gm, rg = data["gmres_iters"], ref["gmres_iters"]
+    assert len(gm) == len(rg)
+    assert all((a is None and b is None) or abs(a - b) <= 1 for a, b in zip(gm, rg))
+    assert data["threshold"] == pytest.approx(ref["threshold"], rel=1e-12)
+    floor = 1e3 * ref["threshold"]
+    for a, b in zip(data["residual_history"], ref["residual_history"]):
+        if b > floor:
+            assert a == pytest.approx(b, rel=1e-8)
+    grid = Grid(cfg.n)
+    if ref["converged"]:
+        for name in ("y.csv", "p.csv", "u.csv"):
+            (tmp_path / f"ref_{name}").write_text(str(g[f"{tag}__{name}"]))
+            assert rel_l2(read_field_csv(tmp_path / name, grid),
+                          read_field_csv(tmp_path / f"ref_{name}", grid)) <= 1e-8, name
+    assert json.loads((tmp_path / "report.json").read_text()) == data
+
+
+@pytest.mark.parametrize("tag", ["raspen_eps", "newton_ras_eps", "newton_eps"])
+def test_run_single_deterministic_modulo_timing(tag, tmp_path):
+    cfg = ExperimentConfig(**{**MILD, **CASES[tag]})
+    _, first = run_single(cfg, tmp_path / "a")
+    _, second = run_single(cfg, tmp_path / "b")
+    first.pop("timing")
+    second.pop("timing")
+    assert first == second
+    for name in ("residual_history.csv", "y.csv", "p.csv", "u.csv"):
+        assert (tmp_path / "a" / name).read_text() == (tmp_path / "b" / name).read_text()
