@@ -121,6 +121,28 @@ def test_baseline_config_ras_solve_matches_reference(name):
     assert rel_l2(u, g["u"]) <= 1e-8
 
 
+@pytest.mark.parametrize("name", ["cfg3", "cfg4"])
+def test_large_config_ras_solve_matches_reference(name):
+    """Configs 3 (expm1, 8x8) and 4 (headline grid, 16x16): the reference's
+    newton-ras-eps record (ras_cfg3: 8 min, ras_cfg4: CPU hours) vs the device."""
+    g = golden(f"ras_{name}.npz")
+    cfg = CONFIGS[name]
+    spec = build_spec(cfg, with_matrix=False)
+    dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    x, rep = newton_ras_solve(np.zeros(cfg.unknowns), dec, spec,
+                              ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min), ras_cfg())
+    assert rep.converged == bool(g["converged"])
+    assert rep.outer_iters == int(g["outer_iters"])
+    assert rep.alphas == list(g["alphas"])
+    assert all(abs(a - b) <= 1 for a, b in zip(rep.gmres_iters, list(g["gmres_iters"])))
+    n2 = cfg.n * cfg.n
+    u = recover_control(x[n2:], spec, cfg.eps_min)
+    for key, vec in (("y", x[:n2]), ("p", x[n2:]), ("u", u)):
+        stride = int(g[f"{key}_stride"])
+        assert rel_l2(vec[::stride], g[f"{key}_samples"]) <= 1e-8, key
+        assert abs(np.linalg.norm(vec) - float(g[f"{key}_norm"])) <= 1e-8 * float(g[f"{key}_norm"])
+
+
 def test_fused_preconditioned_gmres_matches_python_gmres():
     """The native left-preconditioned GMRES and the generic device GMRES
     (krylov.gmres with the same operator and preconditioner) agree."""

@@ -202,6 +202,20 @@ def test_cfg3_reference_settings_fail_like_the_reference():
     np.testing.assert_array_equal(x, np.zeros(cfg.unknowns))
 
 
+def test_cfg4_reference_settings_fail_like_the_reference():
+    """The headline config at the reference's own inner_tol = 1e-8: the
+    reference fails in the third RAS evaluation with subdomain 39 stalling at
+    the FP64 residual floor (tests/golden/cfg4_tol1e-08.npz, 56 min on the CPU);
+    the GPU path reproduces the same record."""
+    g = golden("cfg4_tol1e-08.npz")
+    cfg, x, rep = _solve_cfg("cfg4", 1e-8)
+    assert not rep.converged and not bool(g["converged"])
+    assert rep.failure == str(g["failure"])
+    assert rep.outer_iters == int(g["outer_iters"])
+    assert rep.inner_iters == list(g["inner_iters"])
+    np.testing.assert_array_equal(x, np.zeros(cfg.unknowns))
+
+
 @pytest.mark.parametrize("name", ["cfg5u", "cfg5"])
 def test_cfg5_sweep_and_jvp_match_reference(name):
     from paper_2411_00546_b200.schwarz import _jvp, _sweep
