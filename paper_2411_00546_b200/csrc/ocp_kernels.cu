@@ -89,7 +89,7 @@ __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const dou
 // residual tile goes back through shared memory to be stored in local order.
 constexpr int RT = 32;   // tile edge (oriented points)
 
-__global__ void __launch_bounds__(256) k_residual(const SubInfo* subs, const int* list, Phys P,
+__global__ void __launch_bounds__(256, 4) k_residual(const SubInfo* subs, const int* list, Phys P,
                                                   const double* x, const double* Vpool,
                                                   const double* Dpool, const double* alpha,
                                                   const double* f, const double* yd, double eps,
@@ -130,13 +130,35 @@ __global__ void __launch_bounds__(256) k_residual(const SubInfo* subs, const int
         ydv[u] = yd[g];
       }
     }
-    // 1. stage the halo tile (local order, coalesced along b)
-    for (int e = threadIdx.x; e < (RT + 2) * (RT + 2); e += blockDim.x) {
-      const int ta = e / (RT + 2), tbb = e - ta * (RT + 2);
-      const int la = a0 + ta - 1, lb = b0 + tbb - 1;
-      double2 v = make_double2(0.0, 0.0);
-      if (la >= 0 && la < s.nr && lb >= 0 && lb < s.nc) v = lval(V, D, al, la * s.nc + lb);
-      tv[e] = v;
+    // 1. stage the halo tile (local order, coalesced along b); all loads of
+    //    this thread are issued before the first use (latency overlap)
+    {
+      constexpr int HALO = (RT + 2) * (RT + 2);
+      constexpr int PER = (HALO + 255) / 256;
+      double2 hv[PER], hd[PER];
+      unsigned inmask = 0u;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = threadIdx.x + 256 * u;
+        const int ta = e / (RT + 2), tbb = e - ta * (RT + 2);
+        const int la = a0 + ta - 1, lb = b0 + tbb - 1;
+        const bool in = e < HALO && la >= 0 && la < s.nr && lb >= 0 && lb < s.nc;
+        inmask |= in ? (1u << u) : 0u;
+        hv[u] = in ? V[la * s.nc + lb] : make_double2(0.0, 0.0);
+        hd[u] = (in && D) ? D[la * s.nc + lb] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int e = threadIdx.x + 256 * u;
+        if (e < HALO) {
+          double2 v = hv[u];
+          if (D && (inmask >> u & 1u)) {
+            v.x = add(v.x, mul(al, hd[u].x));
+            v.y = add(v.y, mul(al, hd[u].y));
+          }
+          tv[e] = v;
+        }
+      }
     }
     __syncthreads();
     // 2. evaluate, threads fast along the global column
