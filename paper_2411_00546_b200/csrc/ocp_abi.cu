@@ -21,7 +21,7 @@
 #include "ocp_kernels.cuh"
 
 using namespace ocp;
-namespace ocp { void read_phase(unsigned long long* out); }
+namespace ocp { void read_phase(unsigned long long* out); void read_bphase(unsigned long long* out); }
 
 namespace {
 
@@ -59,6 +59,13 @@ struct ocp_ctx {
   long long* d_bad = nullptr;
   double* scratch = nullptr;
   long long ws_stride = 0;
+  int fmt = 1;                 // factor format: 0 banded LU, 1 block tridiagonal (ocp_block.cu)
+  int maxNPB = 0, maxNPS = 0;
+  int* d_flist = nullptr;      // block format: factor list ordered by decreasing cost
+  int* h_flist = nullptr;
+  double* bscratch = nullptr;  // block format: global Schur blocks too large for shared memory
+  long long bs_stride = 0;
+  int bf_grid = 1;
   int lu_grid = 1, num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
@@ -224,11 +231,45 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   double flops = 0;
   for (int i : list) flops += ctx->sub_flops[i];
   Timer t(ctx, CLS_FACTOR, flops);
+  if (ctx->fmt == 1) {
+    // persistent CTAs take subdomains in list order: largest work first
+    // (global-memory Schur blocks, then nr * NPB^3), so the tail is short
+    if (!ctx->d_flist) {
+      CK(cudaMalloc(&ctx->d_flist, ctx->I * sizeof(int)));
+      CK(cudaMallocHost(&ctx->h_flist, ctx->I * sizeof(int)));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));   // h_flist may still feed a previous copy
+    std::vector<int> ord(list);
+    auto cost = [&](int i) {
+      const SubInfo& su = ctx->subs[i];
+      const double c = (double)su.nr * su.pad_ * su.pad_ * su.pad_;
+      return su.pad_ > BF_SMEM_MAX_NPB ? 4.0 * c : c;
+    };
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
+    for (int i = 0; i < cnt; ++i) ctx->h_flist[i] = ord[i];
+    CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, cnt * sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    const int grid = std::min(cnt, ctx->bf_grid);
+    k_block_factor<<<grid, 256, block_factor_smem_bytes(ctx->maxNPB), ctx->stream>>>(
+        ctx->d_subs, ctx->d_flist, cnt, ctx->P, ctx->JD, fac, ctx->bscratch, ctx->bs_stride,
+        ctx->d_status);
+    CKL();
+    return OCP_OK;
+  }
   const int grid = std::min(cnt, ctx->lu_grid);
   k_band_factor<<<grid, LU_THREADS, factor_smem_bytes(ctx->maxW), ctx->stream>>>(
       ctx->d_subs, d_list, cnt, ctx->P, ctx->JD, fac, ctx->scratch, ctx->ws_stride, ctx->d_status);
   CKL();
   return OCP_OK;
+}
+
+cudaError_t any_solve(ocp_ctx* ctx, int mode, int cnt, const int* d_list, const double* fac,
+                      const double* in, double scale, double* out) {
+  if (ctx->fmt == 1)
+    return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out,
+                              ctx->P.off, ctx->maxNPS);
+  return launch_band_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out,
+                           ctx->maxW);
 }
 
 int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, const double* fac,
@@ -238,7 +279,7 @@ int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, 
   double bytes = 0;
   for (int i : list) bytes += ctx->sub_fbytes[i];
   Timer t(ctx, cls, 0, bytes);
-  CK(launch_band_solve(0, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out, ctx->maxW));
+  CK(any_solve(ctx, 0, cnt, d_list, fac, in, scale, out));
   ++ctx->launches;
   return OCP_OK;
 }
@@ -309,6 +350,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->P.kappa = kappa;
   ctx->P.kappa2 = kappa * kappa;
   long long loc = 0, fac = 0, ref = 0;
+  if (const char* e = getenv("OCP_FACTOR_FORMAT")) ctx->fmt = (std::string(e) == "band") ? 0 : 1;
   for (auto& r : rt) {
     for (auto& c : ct) {
       SubInfo s{};
@@ -327,22 +369,32 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       s.W = std::max(((s.w + NB - 1) / NB) * NB, NBF);
       s.N = 2 * R * C;
       s.NP = ((s.N + NBF - 1) / NBF) * NBF;
+      s.pad_ = ((2 * s.nc + 31) / 32) * 32;   // NPB (Gauss-Jordan panels of 32)
+      s.NPS = ((2 * s.nc + 15) / 16) * 16;    // stored S_a^{-1} (solve chunks of 16 rows)
       s.loc = loc;
       s.fac = fac;
       s.ref = ref;
       loc += s.NP;
-      fac += (long long)s.NP * 2 * (s.W + 1);
       ref += s.N;
       ctx->subs.push_back(s);
       ctx->sub_flops.push_back(band_lu_flops(s.N, s.w));
-      ctx->sub_fbytes.push_back(8.0 * (double)s.N * (2.0 * s.w + 1.0));
-      {
-        // the JVP needs x only on the ownership block: the backward sweep
-        // stops at its first oriented row (k_band_solve MODE 1)
-        const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+      // the JVP needs x only on the ownership block: the backward sweep stops
+      // at its first oriented line (MODE 1 of both solve kernels)
+      const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+      if (ctx->fmt == 0) {
+        fac += (long long)s.NP * 2 * (s.W + 1);
+        ctx->sub_fbytes.push_back(8.0 * (double)s.N * (2.0 * s.w + 1.0));
         const double kstop = 2.0 * s.nc * a_own;
         ctx->sub_jbytes.push_back(8.0 * ((double)s.N * s.w + ((double)s.N - kstop) * (s.w + 1.0)));
+      } else {
+        // S_a^{-1} per line: forward reads all nr, backward nr-1-a_stop of them
+        const double blk = 8.0 * (double)s.NPS * s.NPS;
+        fac += (long long)s.nr * s.NPS * s.NPS;
+        ctx->sub_fbytes.push_back(blk * (2.0 * s.nr - 1.0));
+        ctx->sub_jbytes.push_back(blk * (s.nr + std::max(0, s.nr - 1 - a_own)));
       }
+      ctx->maxNPB = std::max(ctx->maxNPB, s.pad_);
+      ctx->maxNPS = std::max(ctx->maxNPS, s.NPS);
       ctx->sub_dofs.push_back(s.N);
       ctx->maxW = std::max(ctx->maxW, s.W);
       ctx->maxNP = std::max(ctx->maxNP, s.NP);
@@ -418,8 +470,15 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     if (const char* e = getenv("OCP_LU_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));
     ctx->lu_grid = std::min(I, per_sm * ctx->num_sms);
   }
-  ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
-  CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
+  if (ctx->fmt == 0) {
+    ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
+    CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
+  }
+  ctx->bf_grid = std::max(1, std::min(I, ctx->num_sms));
+  if (ctx->fmt == 1 && ctx->maxNPB > BF_SMEM_MAX_NPB) {
+    ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
+    CKC(cudaMalloc(&ctx->bscratch, ctx->bf_grid * ctx->bs_stride * sizeof(double)));
+  }
   CKC(cudaMalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
   CKC(cudaMalloc(&ctx->red_counter, sizeof(unsigned int)));
   CKC(cudaMemset(ctx->red_counter, 0, sizeof(unsigned int)));
@@ -450,6 +509,14 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       return cleanup_fail(OCP_ERR_UNSUPPORTED);
     }
     CKC(set_band_solve_smem(solve_smem));
+    if (ctx->fmt == 1) {
+      const int fb = block_factor_smem_bytes(ctx->maxNPB), sb = (int)block_solve_smem_bytes(ctx->maxNPS);
+      if (fb + 1024 > optin || sb + 1024 > optin) {
+        fail(ctx, OCP_ERR_UNSUPPORTED, "block factor needs more shared memory than the device offers");
+        return cleanup_fail(OCP_ERR_UNSUPPORTED);
+      }
+      CKC(set_block_kernel_smem(fb, sb));
+    }
   }
 #undef CKC
   for (auto& s : ctx->subs) {
@@ -470,12 +537,12 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
-                  (void*)ctx->d_gbad,
+                  (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
                   (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
-                  (void*)ctx->gm_hh, (void*)ctx->st_hhist})
+                  (void*)ctx->gm_hh, (void*)ctx->st_hhist, (void*)ctx->h_flist})
     if (p) cudaFreeHost(p);
   for (auto e : ctx->gm_ev) if (e) cudaEventDestroy(e);
   for (auto& e : ctx->pending) {
@@ -731,8 +798,7 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
     double bytes = 0;
     for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
     Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(launch_band_solve(1, I, st, ctx->d_subs, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B,
-                         ctx->maxW));
+    CK(any_solve(ctx, 1, I, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B));
     ++ctx->launches;
   }
   k_jvp_out<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B, out);
@@ -1002,8 +1068,7 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out)
     double bytes = 0;
     for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
     Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(launch_band_solve(1, I, st, ctx->d_subs, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B,
-                         ctx->maxW));
+    CK(any_solve(ctx, 1, I, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B));
     ++ctx->launches;
   }
   k_ras_out<<<dim3(I, 4), 256, 0, st>>>(ctx->d_subs, ctx->P, ctx->B, out);
@@ -1338,7 +1403,7 @@ int ocp_reset_stats(ocp_ctx* ctx) {
 }
 
 #ifdef OCP_PHASE_TIMING
-int ocp_debug_phase(unsigned long long* out) { ocp::read_phase(out); return 0; }
+int ocp_debug_phase(unsigned long long* out) { ocp::read_phase(out); ocp::read_bphase(out + 8); return 0; }
 #endif
 
 int ocp_event_record(ocp_ctx* ctx, int slot) {

@@ -1,0 +1,501 @@
+// Block-tridiagonal ("block-Thomas") factorisation of the local Jacobians and
+// the matching stored-factor solve (sm_100a, FP64 tensor cores).
+//
+// In band order (k = a*n + t, n = 2 nc, t = 2b + f) the local pair Jacobian
+// (schwarz.py:166-171, system.py:135-144) is block tridiagonal along the long
+// side: diagonal blocks D_a (one grid line: diag, y<->p coupling, +-1
+// neighbours in the line) and off-diagonal blocks off*I (the a +- 1 lines).
+// Its LU without pivoting, grouped by lines, is
+//     S_0 = D_0,   S_a = D_a - off^2 S_{a-1}^{-1},
+// and a solve is
+//     forward   w_a = S_a^{-1} (r_a - off w_{a-1})
+//     backward  x_a = w_a - off S_a^{-1} x_{a+1}.
+// The factor store keeps every S_a^{-1} (n x n, padded to NPS = round16(n),
+// identity on the padding) in COLUMN-major order: half the bytes of the band
+// factors, the same bytes per solve, and the solve becomes dense mat-vecs in
+// which every thread owns one output row (no reductions).  The factor runs
+// the recursion on the transposes, S_a^T = D_a^T - off^2 (S_{a-1}^{-1})^T, so
+// its row-major result is already the column-major S_a^{-1}.
+//
+// k_block_factor: one CTA per subdomain; S stays resident in shared memory
+// (NPB <= 160; larger blocks use a per-CTA global scratch, L2-resident) and is
+// inverted in place by blocked Gauss-Jordan with 32-wide pivot panels:
+//     P1  Pinv = P^{-1} of the 32x32 pivot block (one warp, registers)
+//     P2  S[p, j] = Pinv S[p, j]                       (DMMA, row block)
+//     P3a S[i, j] -= S[i, p] S[p, j]     i, j not in p (DMMA, rank-32)
+//     P3b S[i, p] = -S[i, p] Pinv                      (DMMA, column block)
+// P3b of panel p runs concurrently with P1 of panel p+1.  Every flop except
+// the 32x32 pivot inverses is a DMMA (mma.sync.m8n8k4.f64) on shared-memory
+// operands; nothing round-trips through L2 (the band kernel's bottleneck).
+//
+// k_block_solve<MODE>: one CTA per subdomain; S_a^{-1} streams through a ring
+// of TMA bulk-copy stages in chunks of 16 columns; thread t accumulates
+// output row t; MODE 1 (JVP / RAS apply) stops the backward sweep at the
+// first owned line (schwarz.py:344).
+#include "ocp_kernels.cuh"
+#include "ocp_tma.cuh"
+
+namespace ocp {
+
+constexpr int BF_THREADS = 256;
+
+#ifdef OCP_PHASE_TIMING
+__device__ unsigned long long g_bphase[8];
+#define BPH_START() long long t_last = clock64()
+#define BPH_MARK(k)                                                                     \
+  do {                                                                                  \
+    if (threadIdx.x == 0) {                                                             \
+      const long long now = clock64();                                                  \
+      atomicAdd(&g_bphase[k], (unsigned long long)(now - t_last));                      \
+      t_last = now;                                                                     \
+    }                                                                                   \
+  } while (0)
+void read_bphase(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_bphase, 8 * sizeof(unsigned long long));
+}
+#else
+#define BPH_START() (void)0
+#define BPH_MARK(k) (void)0
+#endif
+constexpr int BS_ROWS = 16;      // rows per solve chunk
+constexpr int BS_STAGES = 4;     // TMA ring depth of the solve
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// entry (i, j) of the diagonal block D_a; JL = the line's Jacobian diagonals
+// (4 per point, copied to shared memory), padding: identity
+__device__ __forceinline__ double d_entry(const SubInfo& s, const double* JL, int i, int j,
+                                          double off) {
+  const int n = 2 * s.nc;
+  if (i >= n || j >= n) return i == j ? 1.0 : 0.0;
+  const int bi = i >> 1, fi = i & 1, bj = j >> 1, fj = j & 1;
+  if (bi == bj) {
+    if (fi == fj) return JL[4 * bi];                   // 4/h^2 + phi'(y)
+    return fi == 0 ? JL[4 * bi + 1] : JL[4 * bi + 2];  // b12 (y row), b21 (p row)
+  }
+  if (fi == fj && (bi - bj == 1 || bj - bi == 1)) return off;
+  return 0.0;
+}
+
+// P1: in-place Gauss-Jordan inverse of the 32x32 block at S[p0.., p0..] by
+// one warp.  Lane j holds column j in registers; the rows are rotated by one
+// position per pivot step so that the pivot row is always c[0] - the pivot
+// loop stays a runtime loop (compact code) with no dynamic register indexing,
+// and nothing goes through memory between steps.  After 32 steps the
+// rotation is back to the identity.
+// reciprocal without the IEEE slow path (no call => nothing spills around
+// it): MUFU seed + two Newton steps, ~1 ulp; pivots are O(1/h^2) normals
+__device__ __forceinline__ double rcp64(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// P1: in-place Gauss-Jordan inverse of the 32x32 block at S[p0.., p0..] by
+// PW warps (named barrier 2).  Thread (w, lane) keeps rows 8w..8w+7 of
+// column `lane` in registers; every pivot step reads the pivot column / row
+// from one of two ping-pong 32x33 buffers and writes its updated entries to
+// the other, so a step costs one barrier.  No shuffles: inside a
+// warp-uniform branch the compiler wraps each shfl in a convergence check.
+constexpr int PW = 4;
+constexpr int WLD = 33;
+__device__ __noinline__ void pivot_inverse32(double* S, int lds, int p0, double* W0, double* W1,
+                                             int wsub, int lane, int* bad) {
+  constexpr int R = 32 / PW;
+  double c[R];
+  double* B = S + p0 * lds + p0;
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    c[i] = B[(R * wsub + i) * lds + lane];
+    W0[(R * wsub + i) * WLD + lane] = c[i];
+  }
+  asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
+  bool ok = true;
+#pragma unroll 1
+  for (int k = 0; k < 32; ++k) {
+    const double* Wr = (k & 1) ? W1 : W0;
+    double* Ww = (k & 1) ? W0 : W1;
+    const double piv = Wr[k * WLD + k];
+    const double ck = Wr[k * WLD + lane];
+    double f[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) f[i] = Wr[(R * wsub + i) * WLD + k];
+    ok = ok && piv != 0.0 && isfinite(piv);
+    const double rp = rcp64(piv);
+    const bool me = lane == k;
+    const double m = me ? rp : ck * rp;   // the new row-k entry of this column
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int row = R * wsub + i;
+      c[i] = row == k ? m : fma(-f[i], m, me ? 0.0 : c[i]);
+      Ww[row * WLD + lane] = c[i];
+    }
+    asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
+  if (!ok) *bad = 1;
+}
+
+// one 32x16 DMMA tile: C (+)= sgn * A[32 x 32] * B[32 x 16]
+//   A element (m, k) at A + m*lda + k ; B element (k, n) at B + k*ldb + n
+__device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
+                                           double c[4][2][2], int lane, double sgn) {
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 4) {
+    const double b0 = B[(kk + t4) * ldb + g];
+    const double b1 = B[(kk + t4) * ldb + 8 + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const double am = sgn * A[(8 * mi + g) * lda + kk + t4];
+      dmma(c[mi][0][0], c[mi][0][1], am, b0);
+      dmma(c[mi][1][0], c[mi][1][1], am, b1);
+    }
+  }
+}
+
+// C tile (32 x 16) at (i0, j0) -> registers / back
+__device__ __forceinline__ void load_c(const double* S, int lds, int i0, int j0, double c[4][2][2],
+                                       int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni) {
+      const double2 v = *reinterpret_cast<const double2*>(S + (i0 + 8 * mi + g) * lds + j0 + 8 * ni + 2 * t4);
+      c[mi][ni][0] = v.x;
+      c[mi][ni][1] = v.y;
+    }
+}
+__device__ __forceinline__ void store_c(double* S, int lds, int i0, int j0, const double c[4][2][2],
+                                        int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 2; ++ni)
+      *reinterpret_cast<double2*>(S + (i0 + 8 * mi + g) * lds + j0 + 8 * ni + 2 * t4) =
+          make_double2(c[mi][ni][0], c[mi][ni][1]);
+}
+
+// P3a tile: S[i0.., j0..] -= S[i0.., p0..p0+32) S[p0.., j0..]
+__device__ __forceinline__ void trailing_tile(double* S, int lds, int i0, int j0, int p0, int lane) {
+  double c[4][2][2];
+  load_c(S, lds, i0, j0, c, lane);
+  tile_32x16(S + i0 * lds + p0, lds, S + p0 * lds + j0, lds, c, lane, -1.0);
+  store_c(S, lds, i0, j0, c, lane);
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, double off,
+                                           double* S, int lds, double* fac, int* bad, double* W0,
+                                           double* W1, int* tile_ctr, double* JL) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BF_THREADS / 32;
+  const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr;
+  const int npan = NPB / 32, nct = NPB / 16;
+  const double mo2 = -(off * off);
+  const long long bsz = (long long)NPS * NPS;   // stored block (rows/cols >= n are identity/zero)
+  BPH_START();
+  // the Jacobian diagonals of the next line are loaded one line ahead
+  // (registers) and staged in shared memory (JL) at the start of its E phase
+  const int nq = 4 * s.nc;
+  double jn0 = tid < nq ? JD[tid] : 0.0, jn1 = tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
+  for (int a = 0; a < nr; ++a) {
+    if (tid < nq) JL[tid] = jn0;
+    if (tid + BF_THREADS < nq) JL[tid + BF_THREADS] = jn1;
+    if (a + 1 < nr) {
+      const double* nx = JD + (long long)(a + 1) * nq;
+      jn0 = tid < nq ? nx[tid] : 0.0;
+      jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
+    }
+    __syncthreads();
+    // ---- E1. store S_{a-1}^{-1} (streaming) and scale: S = -off^2 S_{a-1}^{-1}
+    //      on the real block, identity on the padding (double2 granularity)
+    {
+      double* prev = fac + (long long)(a - 1) * bsz;
+      const int half = NPB / 2;
+      for (int e = tid; e < NPB * half; e += BF_THREADS) {
+        const int i = e / half, j = 2 * (e - i * half);
+        double2* sp = reinterpret_cast<double2*>(S + i * lds + j);
+        const double2 old = *sp;
+        if (a > 0 && i < NPS && j < NPS)
+          __stcs(reinterpret_cast<double2*>(prev + (long long)i * NPS + j), old);
+        double2 v;
+        if (i < n) {
+          v.x = j < n ? (a > 0 ? mo2 * old.x : 0.0) : (i == j ? 1.0 : 0.0);
+          v.y = j + 1 < n ? (a > 0 ? mo2 * old.y : 0.0) : (i == j + 1 ? 1.0 : 0.0);
+        } else {
+          v.x = i == j ? 1.0 : 0.0;
+          v.y = i == j + 1 ? 1.0 : 0.0;
+        }
+        *sp = v;
+      }
+    }
+    __syncthreads();
+    // ---- E2. + D_a: five diagonals (i - j in [-2, 2]) of the real block;
+    //      then P1 of panel 0 (warps 0..PW-1)
+    for (int e = tid; e < 5 * n; e += BF_THREADS) {
+      const int i = e / 5, j = i + (e - 5 * i) - 2;
+      if (j >= 0 && j < n) S[i * lds + j] += d_entry(s, JL, j, i, off);   // transposed
+    }
+    __syncthreads();
+    if (warp < PW) pivot_inverse32(S, lds, 0, W0, W1, warp, lane, bad);
+    __syncthreads();
+    BPH_MARK(1);
+    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels
+    for (int p = 0; p < npan; ++p) {
+      const int p0 = 32 * p;
+      const double* Pinv = S + p0 * lds + p0;
+      // ---- P2: row block S[p, j] = Pinv S[p, j] (column tiles of 16 outside p)
+      if (tid == 0) *tile_ctr = 0;
+      for (int ct = warp; ct < nct; ct += NW) {
+        if (ct == 2 * p || ct == 2 * p + 1) continue;
+        const int j0 = 16 * ct;
+        double c[4][2][2] = {};
+        tile_32x16(Pinv, lds, S + p0 * lds + j0, lds, c, lane, 1.0);
+        store_c(S, lds, p0, j0, c, lane);
+      }
+      __syncthreads();
+      BPH_MARK(2);
+      // ---- P3a (rank-32 trailing update) with lookahead: warps 0,1 first
+      //      update the next pivot block S[p+1, p+1]; warps 0..PW-1 then
+      //      invert it (P1 of p+1) while the other warps start on the other
+      //      trailing tiles, which everybody pulls from a shared counter.
+      const bool la = p + 1 < npan;
+#ifdef OCP_PHASE_TIMING
+      long long tw0 = clock64();
+#endif
+      if (warp < PW) {
+        if (la && warp < 2) trailing_tile(S, lds, p0 + 32, p0 + 32 + 16 * warp, p0, lane);
+        if (la) {
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
+#ifndef OCP_EXP_NO_P1
+          pivot_inverse32(S, lds, p0 + 32, W0, W1, warp, lane, bad);
+#endif
+        }
+      }
+#ifdef OCP_PHASE_TIMING
+      long long tw1 = clock64();
+#endif
+      {
+        const int nrt = npan - 1, ncw = nct - 2, total = nrt * ncw;
+#ifdef OCP_EXP_STATIC
+        for (int tI = warp; tI < total; tI += NW) {
+#else
+        for (;;) {
+          int tI = 0;
+          if (lane == 0) tI = atomicAdd(tile_ctr, 1);
+          tI = __shfl_sync(0xffffffffu, tI, 0);
+          if (tI >= total) break;
+#endif
+          int rt = tI / ncw, ct = tI - rt * ncw;
+          rt += rt >= p ? 1 : 0;
+          ct += ct >= 2 * p ? 2 : 0;
+          if (la && rt == p + 1 && (ct == 2 * p + 2 || ct == 2 * p + 3)) continue;  // lookahead tiles
+#ifdef OCP_PHASE_TIMING
+          long long tt0 = clock64();
+#endif
+          trailing_tile(S, lds, 32 * rt, 16 * ct, p0, lane);
+#ifdef OCP_PHASE_TIMING
+          if (lane == 0) {
+            atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tt0));
+            atomicAdd(&g_bphase[4 + 0 * 0], 0ull);
+          }
+#endif
+        }
+      }
+#ifdef OCP_PHASE_TIMING
+      if (lane == 0 && warp == 0) {
+        atomicAdd(&g_bphase[5], (unsigned long long)(tw1 - tw0));
+        atomicAdd(&g_bphase[6], (unsigned long long)(clock64() - tw1));
+      }
+      if (lane == 0 && warp == PW) atomicAdd(&g_bphase[7], (unsigned long long)(clock64() - tw1));
+#endif
+      __syncthreads();
+      BPH_MARK(3);
+      // ---- P3b: column block S[i, p] = -S[i, p] Pinv (one warp per row tile)
+      for (int rt = warp; rt < npan; rt += NW) {
+        if (rt == p) continue;
+        const int i0 = 32 * rt;
+        double c0[4][2][2] = {}, c1[4][2][2] = {};
+        tile_32x16(S + i0 * lds + p0, lds, Pinv, lds, c0, lane, -1.0);
+        tile_32x16(S + i0 * lds + p0, lds, Pinv + 16, lds, c1, lane, -1.0);
+        store_c(S, lds, i0, p0, c0, lane);
+        store_c(S, lds, i0, p0 + 16, c1, lane);
+      }
+      __syncthreads();
+      BPH_MARK(4);
+    }
+#ifndef OCP_EXP_IGNORE_BAD
+    if (*bad) return;
+#endif
+  }
+  // the last S^{-1}
+  double* last = fac + (long long)(nr - 1) * bsz;
+  for (int i = warp; i < NPS; i += NW)
+    for (int j = lane; j < NPS; j += 32) __stcs(last + (long long)i * NPS + j, S[i * lds + j]);
+}
+
+__global__ void __launch_bounds__(BF_THREADS, 1)
+k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const double* JDpool,
+               double* fac_pool, double* gscratch, long long gs_stride, int* status) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int bad;
+  __shared__ int tile_ctr;
+  for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+    const int sid = list[li];
+    const SubInfo s = subs[sid];
+    const double* JD = JDpool + 2 * s.loc;
+    double* fac = fac_pool + s.fac;
+    const int lds = s.pad_ + 4;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    // shared memory: [S (if resident)][W0][W1] (pivot ping-pong buffers)
+    const int sres = s.pad_ <= BF_SMEM_MAX_NPB ? s.pad_ * lds : 0;
+    double* W0 = sm + BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4);
+    double* W1 = W0 + 32 * WLD;
+    double* JL = W1 + 32 * WLD;
+    (void)sres;
+    if (s.pad_ <= BF_SMEM_MAX_NPB)
+      factor_one<true>(s, JD, P.off, sm, lds, fac, &bad, W0, W1, &tile_ctr, JL);
+    else
+      factor_one<false>(s, JD, P.off, gscratch + (long long)blockIdx.x * gs_stride, lds, fac, &bad,
+                        W0, W1, &tile_ctr, JL);
+    __syncthreads();
+    if (threadIdx.x == 0) status[sid] = bad;
+    __syncthreads();
+  }
+}
+
+int block_factor_smem_bytes(int max_npb) {
+  (void)max_npb;   // fixed layout: [S: 160 x 164][W0, W1: 32 x 33]
+  return (int)sizeof(double) * (BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4) + 2 * 32 * WLD + 4 * 112);
+}
+
+// ---------------------------------------------------------------------------
+// solve with the stored S_a^{-1}
+// ---------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(256)
+k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
+              double scale, double* out_pool, double off, int max_npb) {
+  extern __shared__ __align__(16) double sm[];
+  const SubInfo s = subs[list[blockIdx.x]];
+  const int tid = threadIdx.x;
+  const int NPB = s.NPS, n = 2 * s.nc, nr = s.nr;   // stored block size (multiple of 16)
+  const int SB = BS_ROWS * NPB;                       // doubles per stage
+  double* stage = sm;                                 // [BS_STAGES][BS_ROWS][NPB]
+  double* vin = sm + BS_STAGES * BS_ROWS * max_npb;   // mat-vec input of the current line
+  __shared__ __align__(8) uint64_t bars[BS_STAGES];
+  const double* fac = fac_pool + s.fac;
+  const double* in = in_pool + s.loc;
+  double* out = out_pool + s.loc;
+  const long long bsz = (long long)NPB * NPB;
+  const int cpb = NPB / BS_ROWS;                      // chunks per line
+  int a_stop = 0;
+  if (MODE == 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+  const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;   // lines a = nr-2 .. a_stop
+  const int total = (nr + nback) * cpb;
+  auto chunk_src = [&](int t) -> const double* {
+    const int blk = t / cpb, c = t - blk * cpb;
+    const int a = blk < nr ? blk : nr - 2 - (blk - nr);
+    return fac + a * bsz + (long long)c * SB;
+  };
+  const uint32_t bytes = (uint32_t)(SB * sizeof(double));
+  if (tid == 0) {
+    for (int i = 0; i < BS_STAGES; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int t = 0; t < BS_STAGES && t < total; ++t) {
+      mbar_expect_tx(&bars[t], bytes);
+      bulk_g2s(stage + t * SB, chunk_src(t), bytes, &bars[t]);
+    }
+  }
+  // line 0 input
+  for (int t = tid; t < NPB; t += blockDim.x) vin[t] = t < n ? scale * in[t] : 0.0;
+  __syncthreads();
+  int t = 0;
+  // thread `tid` owns output row tid of every line (tid < NPB)
+  for (int blk = 0; blk < nr + nback; ++blk) {
+    const bool fwd = blk < nr;
+    const int a = fwd ? blk : nr - 2 - (blk - nr);
+    // prefetch of this thread's combine operand (in_{a+1} forward, w_a backward)
+    double nxt = 0.0;
+    if (tid < n) {
+      if (fwd) {
+        if (a + 1 < nr) nxt = in[(long long)(a + 1) * n + tid];
+      } else {
+        nxt = out[(long long)a * n + tid];
+      }
+    }
+    double y0 = 0.0, y1 = 0.0;
+    for (int c = 0; c < cpb; ++c, ++t) {
+      const int st = t % BS_STAGES;
+      mbar_wait(&bars[st], (t / BS_STAGES) & 1);
+      const double* ch = stage + st * SB;   // columns c*16 .. c*16+15 of S_a^{-1}
+      if (tid < NPB) {
+        const double* vc = vin + c * BS_ROWS;
+#pragma unroll
+        for (int cc = 0; cc < BS_ROWS; cc += 2) {
+          y0 = fma(ch[cc * NPB + tid], vc[cc], y0);
+          y1 = fma(ch[(cc + 1) * NPB + tid], vc[cc + 1], y1);
+        }
+      }
+      __syncthreads();
+      if (tid == 0 && t + BS_STAGES < total) {
+        mbar_expect_tx(&bars[st], bytes);
+        bulk_g2s(stage + st * SB, chunk_src(t + BS_STAGES), bytes, &bars[st]);
+      }
+    }
+    const double y = y0 + y1;   // (S_a^{-1} vin)[tid]
+    if (tid < NPB) {
+      if (fwd) {
+        // w_a = y; next input = scale in_{a+1} - off w_a (the last line starts
+        // the backward sweep with x_{nr-1} = w_{nr-1})
+        const double w = tid < n ? y : 0.0;
+        if (tid < n) out[(long long)a * n + tid] = w;
+        vin[tid] = (a + 1 < nr) ? (tid < n ? fma(-off, w, scale * nxt) : 0.0) : w;
+      } else {
+        // x_a = w_a - off y ; next input = x_a
+        const double x = tid < n ? fma(-off, y, nxt) : 0.0;
+        if (tid < n) out[(long long)a * n + tid] = x;
+        vin[tid] = x;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+size_t block_solve_smem_bytes(int max_npb) {
+  return sizeof(double) * ((size_t)BS_STAGES * BS_ROWS * max_npb + 2 * (size_t)max_npb);
+}
+
+cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
+                               const int* list, const double* fac, const double* in, double scale,
+                               double* out_pool, double off, int max_npb) {
+  const size_t smem = block_solve_smem_bytes(max_npb);
+  if (mode == 0)
+    k_block_solve<0><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+  else
+    k_block_solve<1><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+  return cudaGetLastError();
+}
+
+cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes) {
+  cudaError_t e = cudaFuncSetAttribute(k_block_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       factor_bytes);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_block_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_block_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+}
+
+}  // namespace ocp

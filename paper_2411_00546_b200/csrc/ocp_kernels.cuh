@@ -59,6 +59,16 @@ cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo
                               const int* list, const double* fac, const double* in, double scale,
                               double* out_pool, int max_w);
 cudaError_t set_band_solve_smem(int bytes);
+// block-tridiagonal format (ocp_block.cu)
+__global__ void k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
+                               const double* JDpool, double* fac_pool, double* gscratch,
+                               long long gs_stride, int* status);
+int block_factor_smem_bytes(int max_npb);
+size_t block_solve_smem_bytes(int max_npb);
+cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
+                               const int* list, const double* fac, const double* in, double scale,
+                               double* out_pool, double off, int max_npb);
+cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes);
 // one full MGS Arnoldi step (ocp_krylov.cu); cudaErrorNotSupported if n too large
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
                            long long ldq, int j, const double* w_in, double* partials,
