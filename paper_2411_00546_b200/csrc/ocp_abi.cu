@@ -234,9 +234,9 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   if (ctx->fmt == 1) {
     // persistent CTAs take subdomains in list order: largest work first
     // (global-memory Schur blocks, then nr * NPB^3), so the tail is short
-    if (!ctx->d_flist) {
-      CK(cudaMalloc(&ctx->d_flist, ctx->I * sizeof(int)));
-      CK(cudaMallocHost(&ctx->h_flist, ctx->I * sizeof(int)));
+    if (!ctx->d_flist) {   // list + the work counter of the persistent CTAs
+      CK(cudaMalloc(&ctx->d_flist, (ctx->I + 1) * sizeof(int)));
+      CK(cudaMallocHost(&ctx->h_flist, (ctx->I + 1) * sizeof(int)));
     }
     CK(cudaStreamSynchronize(ctx->stream));   // h_flist may still feed a previous copy
     std::vector<int> ord(list);
@@ -247,7 +247,8 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     };
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
     for (int i = 0; i < cnt; ++i) ctx->h_flist[i] = ord[i];
-    CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, cnt * sizeof(int), cudaMemcpyHostToDevice,
+    ctx->h_flist[cnt] = 0;
+    CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, (cnt + 1) * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
     const int grid = std::min(cnt, ctx->bf_grid);
     k_block_factor<<<grid, 256, block_factor_smem_bytes(ctx->maxNPB), ctx->stream>>>(

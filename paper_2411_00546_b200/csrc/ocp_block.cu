@@ -104,13 +104,12 @@ __device__ __forceinline__ double rcp64(double x) {
 // from one of two ping-pong 32x33 buffers and writes its updated entries to
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
-constexpr int PW = 4;
+constexpr int PW = 8;   // all warps of the CTA
 constexpr int WLD = 33;
-__device__ __noinline__ void pivot_inverse32(double* S, int lds, int p0, double* W0, double* W1,
-                                             int wsub, int lane, int* bad) {
+__device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
+                                             int lane, int* bad) {
   constexpr int R = 32 / PW;
   double c[R];
-  double* B = S + p0 * lds + p0;
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     c[i] = B[(R * wsub + i) * lds + lane];
@@ -142,6 +141,18 @@ __device__ __noinline__ void pivot_inverse32(double* S, int lds, int p0, double*
 #pragma unroll
   for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
   if (!ok) *bad = 1;
+#ifdef OCP_EXP_COUNT_SUB
+  {
+    int sub = 0, tiny = 0;
+    for (int i = 0; i < R; ++i) {
+      const double v = fabs(c[i]);
+      sub += (v != 0.0 && v < 2.2250738585072014e-308);
+      tiny += (v != 0.0 && v < 1e-250);
+    }
+    if (sub) atomicAdd(&g_bphase[6], (unsigned long long)sub);
+    if (tiny) atomicAdd(&g_bphase[7], (unsigned long long)tiny);
+  }
+#endif
 }
 
 // one 32x16 DMMA tile: C (+)= sgn * A[32 x 32] * B[32 x 16]
@@ -162,45 +173,74 @@ __device__ __forceinline__ void tile_32x16(const double* A, int lda, const doubl
   }
 }
 
-// C tile (32 x 16) at (i0, j0) -> registers / back
-__device__ __forceinline__ void load_c(const double* S, int lds, int i0, int j0, double c[4][2][2],
-                                       int lane) {
+// C tile (32 x 16) at base (row stride lds) -> registers / back
+__device__ __forceinline__ void load_c(const double* base, int lds, double c[4][2][2], int lane) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
-      const double2 v = *reinterpret_cast<const double2*>(S + (i0 + 8 * mi + g) * lds + j0 + 8 * ni + 2 * t4);
+      const double2 v = *reinterpret_cast<const double2*>(base + (8 * mi + g) * lds + 8 * ni + 2 * t4);
       c[mi][ni][0] = v.x;
       c[mi][ni][1] = v.y;
     }
 }
-__device__ __forceinline__ void store_c(double* S, int lds, int i0, int j0, const double c[4][2][2],
-                                        int lane) {
+__device__ __forceinline__ void store_c(double* base, int lds, const double c[4][2][2], int lane) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
-      *reinterpret_cast<double2*>(S + (i0 + 8 * mi + g) * lds + j0 + 8 * ni + 2 * t4) =
+      *reinterpret_cast<double2*>(base + (8 * mi + g) * lds + 8 * ni + 2 * t4) =
           make_double2(c[mi][ni][0], c[mi][ni][1]);
 }
 
-// P3a tile: S[i0.., j0..] -= S[i0.., p0..p0+32) S[p0.., j0..]
-__device__ __forceinline__ void trailing_tile(double* S, int lds, int i0, int j0, int p0, int lane) {
-  double c[4][2][2];
-  load_c(S, lds, i0, j0, c, lane);
-  tile_32x16(S + i0 * lds + p0, lds, S + p0 * lds + j0, lds, c, lane, -1.0);
-  store_c(S, lds, i0, j0, c, lane);
+// P3b strip: out[16 x 32] = -A[16 x 32] P  (A and out at the same place)
+__device__ __forceinline__ void strip_16x32(double* A, const double* P, int lds, int lane) {
+  const int g = lane >> 2, t4 = lane & 3;
+  double c[2][4][2] = {};
+#pragma unroll
+  for (int kk = 0; kk < 32; kk += 4) {
+    double b[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = P[(kk + t4) * lds + 8 * ni + g];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const double am = -A[(8 * mi + g) * lds + kk + t4];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(c[mi][ni][0], c[mi][ni][1], am, b[ni]);
+    }
+  }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      *reinterpret_cast<double2*>(A + (8 * mi + g) * lds + 8 * ni + 2 * t4) =
+          make_double2(c[mi][ni][0], c[mi][ni][1]);
 }
 
-template <bool SMEM>
+// Row storage of the Schur block.  Normally every row is in shared memory;
+// blocks larger than the shared capacity keep rows [0, r0) there and the
+// rest in a per-CTA global scratch (L2-resident).  Row tiles are 32-row
+// aligned and r0 is a multiple of 32, so a tile never straddles the split.
+template <bool SPLIT>
+struct Rows {
+  double* s;
+  double* g;
+  int r0, lds;
+  __device__ __forceinline__ double* row(int i) const {
+    if (!SPLIT) return s + i * lds;
+    return i < r0 ? s + i * lds : g + (i - r0) * lds;
+  }
+};
+
+template <bool SPLIT>
 __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, double off,
-                                           double* S, int lds, double* fac, int* bad, double* W0,
-                                           double* W1, int* tile_ctr, double* JL) {
+                                           const Rows<SPLIT> R, double* fac, int* bad, double* W0,
+                                           double* W1, double* JL) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = BF_THREADS / 32;
-  const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr;
+  const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr, lds = R.lds;
   const int npan = NPB / 32, nct = NPB / 16;
   const double mo2 = -(off * off);
   const long long bsz = (long long)NPS * NPS;   // stored block (rows/cols >= n are identity/zero)
@@ -209,6 +249,23 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
   // (registers) and staged in shared memory (JL) at the start of its E phase
   const int nq = 4 * s.nc;
   double jn0 = tid < nq ? JD[tid] : 0.0, jn1 = tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
+  // S^{-1} of a line goes to the factor store by TMA bulk stores (one per
+  // shared row, issued by warp 0): the copies run on the TMA engine, so no
+  // global store traffic sits in the load/store queues of the compute phases
+  auto store_block = [&](int line) {
+    double* dst = fac + (long long)line * bsz;
+    const int rs = SPLIT ? (R.r0 < NPS ? R.r0 : NPS) : NPS;   // rows held in shared memory
+    if (warp == 0) {
+      for (int i = lane; i < rs; i += 32)
+        bulk_s2g(dst + (long long)i * NPS, R.row(i), (uint32_t)(NPS * sizeof(double)));
+      bulk_commit();
+    }
+    if (SPLIT)
+      for (int i = rs + warp; i < NPS; i += NW)
+        for (int j = lane; j < NPS; j += 32) __stcs(dst + (long long)i * NPS + j, R.row(i)[j]);
+    if (warp == 0) bulk_wait_read();
+    __syncthreads();
+  };
   for (int a = 0; a < nr; ++a) {
     if (tid < nq) JL[tid] = jn0;
     if (tid + BF_THREADS < nq) JL[tid + BF_THREADS] = jn1;
@@ -217,18 +274,15 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       jn0 = tid < nq ? nx[tid] : 0.0;
       jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
     }
-    __syncthreads();
-    // ---- E1. store S_{a-1}^{-1} (streaming) and scale: S = -off^2 S_{a-1}^{-1}
-    //      on the real block, identity on the padding (double2 granularity)
+    if (a > 0) store_block(a - 1);
+    else __syncthreads();
+    // ---- E1. S = -off^2 S_{a-1}^{-1} on the real block, identity on the padding
     {
-      double* prev = fac + (long long)(a - 1) * bsz;
       const int half = NPB / 2;
       for (int e = tid; e < NPB * half; e += BF_THREADS) {
         const int i = e / half, j = 2 * (e - i * half);
-        double2* sp = reinterpret_cast<double2*>(S + i * lds + j);
+        double2* sp = reinterpret_cast<double2*>(R.row(i) + j);
         const double2 old = *sp;
-        if (a > 0 && i < NPS && j < NPS)
-          __stcs(reinterpret_cast<double2*>(prev + (long long)i * NPS + j), old);
         double2 v;
         if (i < n) {
           v.x = j < n ? (a > 0 ? mo2 * old.x : 0.0) : (i == j ? 1.0 : 0.0);
@@ -241,117 +295,80 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       }
     }
     __syncthreads();
-    // ---- E2. + D_a: five diagonals (i - j in [-2, 2]) of the real block;
-    //      then P1 of panel 0 (warps 0..PW-1)
+    // ---- E2. + D_a^T: five diagonals of the real block (the recursion runs on
+    //      the transposes so that the stored inverse is column-major)
     for (int e = tid; e < 5 * n; e += BF_THREADS) {
       const int i = e / 5, j = i + (e - 5 * i) - 2;
-      if (j >= 0 && j < n) S[i * lds + j] += d_entry(s, JL, j, i, off);   // transposed
+      if (j >= 0 && j < n) R.row(i)[j] += d_entry(s, JL, j, i, off);
     }
     __syncthreads();
-    if (warp < PW) pivot_inverse32(S, lds, 0, W0, W1, warp, lane, bad);
-    __syncthreads();
     BPH_MARK(1);
-    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels
+    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels; every
+    //      phase runs on all warps (the latency-bound pivot chain slows down
+    //      next to concurrent DMMA traffic)
     for (int p = 0; p < npan; ++p) {
       const int p0 = 32 * p;
-      const double* Pinv = S + p0 * lds + p0;
+      double* Prow = R.row(p0);                 // the pivot row block
+      const double* Pinv = Prow + p0;
+      // ---- P1: Pinv = inverse of the pivot block
+      pivot_inverse32(Prow + p0, lds, W0, W1, warp, lane, bad);
+      __syncthreads();
+      BPH_MARK(5);
       // ---- P2: row block S[p, j] = Pinv S[p, j] (column tiles of 16 outside p)
-      if (tid == 0) *tile_ctr = 0;
-      for (int ct = warp; ct < nct; ct += NW) {
-        if (ct == 2 * p || ct == 2 * p + 1) continue;
-        const int j0 = 16 * ct;
+      for (int tI = warp; tI < nct - 2; tI += NW) {
+        const int j0 = 16 * (tI + (tI >= 2 * p ? 2 : 0));
         double c[4][2][2] = {};
-        tile_32x16(Pinv, lds, S + p0 * lds + j0, lds, c, lane, 1.0);
-        store_c(S, lds, p0, j0, c, lane);
+        tile_32x16(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
+        store_c(Prow + j0, lds, c, lane);
       }
       __syncthreads();
       BPH_MARK(2);
-      // ---- P3a (rank-32 trailing update) with lookahead: warps 0,1 first
-      //      update the next pivot block S[p+1, p+1]; warps 0..PW-1 then
-      //      invert it (P1 of p+1) while the other warps start on the other
-      //      trailing tiles, which everybody pulls from a shared counter.
-      const bool la = p + 1 < npan;
-#ifdef OCP_PHASE_TIMING
-      long long tw0 = clock64();
-#endif
-      if (warp < PW) {
-        if (la && warp < 2) trailing_tile(S, lds, p0 + 32, p0 + 32 + 16 * warp, p0, lane);
-        if (la) {
-          asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
-#ifndef OCP_EXP_NO_P1
-          pivot_inverse32(S, lds, p0 + 32, W0, W1, warp, lane, bad);
-#endif
-        }
-      }
-#ifdef OCP_PHASE_TIMING
-      long long tw1 = clock64();
-#endif
+      // ---- P3a: S[i, j] -= S[i, p] S[p, j]   (i, j outside p)
       {
-        const int nrt = npan - 1, ncw = nct - 2, total = nrt * ncw;
-#ifdef OCP_EXP_STATIC
+        const int ncw = nct - 2, total = (npan - 1) * ncw;
         for (int tI = warp; tI < total; tI += NW) {
-#else
-        for (;;) {
-          int tI = 0;
-          if (lane == 0) tI = atomicAdd(tile_ctr, 1);
-          tI = __shfl_sync(0xffffffffu, tI, 0);
-          if (tI >= total) break;
-#endif
           int rt = tI / ncw, ct = tI - rt * ncw;
           rt += rt >= p ? 1 : 0;
           ct += ct >= 2 * p ? 2 : 0;
-          if (la && rt == p + 1 && (ct == 2 * p + 2 || ct == 2 * p + 3)) continue;  // lookahead tiles
-#ifdef OCP_PHASE_TIMING
-          long long tt0 = clock64();
-#endif
-          trailing_tile(S, lds, 32 * rt, 16 * ct, p0, lane);
-#ifdef OCP_PHASE_TIMING
-          if (lane == 0) {
-            atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tt0));
-            atomicAdd(&g_bphase[4 + 0 * 0], 0ull);
-          }
-#endif
+          double* Ci = R.row(32 * rt);
+          double c[4][2][2];
+          load_c(Ci + 16 * ct, lds, c, lane);
+          tile_32x16(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
+          store_c(Ci + 16 * ct, lds, c, lane);
         }
       }
-#ifdef OCP_PHASE_TIMING
-      if (lane == 0 && warp == 0) {
-        atomicAdd(&g_bphase[5], (unsigned long long)(tw1 - tw0));
-        atomicAdd(&g_bphase[6], (unsigned long long)(clock64() - tw1));
-      }
-      if (lane == 0 && warp == PW) atomicAdd(&g_bphase[7], (unsigned long long)(clock64() - tw1));
-#endif
       __syncthreads();
       BPH_MARK(3);
-      // ---- P3b: column block S[i, p] = -S[i, p] Pinv (one warp per row tile)
-      for (int rt = warp; rt < npan; rt += NW) {
-        if (rt == p) continue;
-        const int i0 = 32 * rt;
-        double c0[4][2][2] = {}, c1[4][2][2] = {};
-        tile_32x16(S + i0 * lds + p0, lds, Pinv, lds, c0, lane, -1.0);
-        tile_32x16(S + i0 * lds + p0, lds, Pinv + 16, lds, c1, lane, -1.0);
-        store_c(S, lds, i0, p0, c0, lane);
-        store_c(S, lds, i0, p0 + 16, c1, lane);
+      // ---- P3b: column block S[i, p] = -S[i, p] Pinv, 16-row strips (each
+      //      warp reads and overwrites only its own rows)
+      for (int st = warp; st < 2 * (npan - 1); st += NW) {
+        int rt = st >> 1;
+        rt += rt >= p ? 1 : 0;
+        strip_16x32(R.row(32 * rt + 16 * (st & 1)) + p0, Pinv, lds, lane);
       }
       __syncthreads();
       BPH_MARK(4);
     }
-#ifndef OCP_EXP_IGNORE_BAD
     if (*bad) return;
-#endif
   }
-  // the last S^{-1}
-  double* last = fac + (long long)(nr - 1) * bsz;
-  for (int i = warp; i < NPS; i += NW)
-    for (int j = lane; j < NPS; j += 32) __stcs(last + (long long)i * NPS + j, S[i * lds + j]);
+  // the last S^{-1}; the factor store must be complete when the kernel ends
+  store_block(nr - 1);
+  if (warp == 0) bulk_wait_all();
 }
 
 __global__ void __launch_bounds__(BF_THREADS, 1)
 k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const double* JDpool,
                double* fac_pool, double* gscratch, long long gs_stride, int* status) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ int bad;
-  __shared__ int tile_ctr;
-  for (int li = blockIdx.x; li < cnt; li += gridDim.x) {
+  __shared__ int bad, next;
+  // dynamic distribution: CTAs take the next subdomain of the (cost-sorted)
+  // list from a counter stored at list[cnt] (zeroed by the host)
+  int* counter = const_cast<int*>(list) + cnt;
+  for (;;) {
+    if (threadIdx.x == 0) next = atomicAdd(counter, 1);
+    __syncthreads();
+    const int li = next;
+    if (li >= cnt) break;
     const int sid = list[li];
     const SubInfo s = subs[sid];
     const double* JD = JDpool + 2 * s.loc;
@@ -359,17 +376,19 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     const int lds = s.pad_ + 4;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
-    // shared memory: [S (if resident)][W0][W1] (pivot ping-pong buffers)
-    const int sres = s.pad_ <= BF_SMEM_MAX_NPB ? s.pad_ * lds : 0;
-    double* W0 = sm + BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4);
+    // shared memory: [S rows: SMEM_S doubles][W0, W1: 32 x 33][JL]
+    constexpr int SMEM_S = BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4);
+    double* W0 = sm + SMEM_S;
     double* W1 = W0 + 32 * WLD;
     double* JL = W1 + 32 * WLD;
-    (void)sres;
-    if (s.pad_ <= BF_SMEM_MAX_NPB)
-      factor_one<true>(s, JD, P.off, sm, lds, fac, &bad, W0, W1, &tile_ctr, JL);
-    else
-      factor_one<false>(s, JD, P.off, gscratch + (long long)blockIdx.x * gs_stride, lds, fac, &bad,
-                        W0, W1, &tile_ctr, JL);
+    if (s.pad_ <= BF_SMEM_MAX_NPB) {
+      factor_one<false>(s, JD, P.off, Rows<false>{sm, nullptr, s.pad_, lds}, fac, &bad, W0, W1, JL);
+    } else {
+      const int r0 = (SMEM_S / lds) / 32 * 32;   // rows that fit in shared memory
+      factor_one<true>(s, JD, P.off,
+                       Rows<true>{sm, gscratch + (long long)blockIdx.x * gs_stride, r0, lds}, fac,
+                       &bad, W0, W1, JL);
+    }
     __syncthreads();
     if (threadIdx.x == 0) status[sid] = bad;
     __syncthreads();

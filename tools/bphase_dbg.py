@@ -11,9 +11,9 @@ lib = ctypes.CDLL("paper_2411_00546_b200/libocpgpu.so")
 buf = (ctypes.c_ulonglong * 16)()
 lib.ocp_debug_phase(buf)
 v = np.array(list(buf), dtype=float)[8:]
-names = ["", "E + first P1", "P2 row block", "P3a + lookahead P1", "P3b column block",
-         "  warp 0: lookahead tile + P1", "  warp 0: tile loop", "  warp 4: tile loop"]
-tot = v[1:5].sum()
-print(f"trailing tile cycles (sum over all warps/tiles): {v[0]:.3e}  per tile: {v[0] / (256 * 79 * 28 * 5):.0f} (approx count)")
+names = ["", "store + E", "P2 row block", "P3a trailing", "P3b column block", "P1 pivot inverse",
+         "P1 subnormal entries (exp)", "P1 entries < 1e-250 (exp)"]
+tot = v[1:6].sum()
+
 for k in range(1, 8):
     print(f"{names[k]:28s} {100 * v[k] / tot:5.1f}%  {v[k]:.3e} cycles")
