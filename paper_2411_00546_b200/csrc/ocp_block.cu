@@ -276,25 +276,42 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     }
     if (a > 0) store_block(a - 1);
     else __syncthreads();
-    // ---- E1. S = -off^2 S_{a-1}^{-1} on the real block, identity on the padding
-    {
-      const int half = NPB / 2;
-      for (int e = tid; e < NPB * half; e += BF_THREADS) {
-        const int i = e / half, j = 2 * (e - i * half);
-        double2* sp = reinterpret_cast<double2*>(R.row(i) + j);
-        const double2 old = *sp;
-        double2 v;
-        if (i < n) {
-          v.x = j < n ? (a > 0 ? mo2 * old.x : 0.0) : (i == j ? 1.0 : 0.0);
-          v.y = j + 1 < n ? (a > 0 ? mo2 * old.y : 0.0) : (i == j + 1 ? 1.0 : 0.0);
-        } else {
-          v.x = i == j ? 1.0 : 0.0;
-          v.y = i == j + 1 ? 1.0 : 0.0;
+    BPH_MARK(6);
+    // ---- E1. S = -off^2 S_{a-1}^{-1} on the real block, identity on the
+    //      padding (warp per row, double2 columns; all loads of a row pair are
+    //      issued before any store)
+    for (int i0 = 2 * warp; i0 < NPB; i0 += 2 * NW) {
+      double2 v[2][4];
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 2 * lane + 64 * u;
+          v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(R.row(i0 + r) + j)
+                                       : make_double2(0.0, 0.0);
         }
-        *sp = v;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int i = i0 + r;
+        double* rw = R.row(i);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 2 * lane + 64 * u;
+          if (j >= NPB) continue;
+          double2 w;
+          if (i < n && j < n) {
+            w.x = mo2 * v[r][u].x;
+            w.y = mo2 * v[r][u].y;
+          } else {
+            w.x = i == j ? 1.0 : 0.0;
+            w.y = i == j + 1 ? 1.0 : 0.0;
+          }
+          *reinterpret_cast<double2*>(rw + j) = w;
+        }
       }
     }
     __syncthreads();
+    BPH_MARK(7);
     // ---- E2. + D_a^T: five diagonals of the real block (the recursion runs on
     //      the transposes so that the stored inverse is column-major)
     for (int e = tid; e < 5 * n; e += BF_THREADS) {

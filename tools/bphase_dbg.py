@@ -11,9 +11,9 @@ lib = ctypes.CDLL("paper_2411_00546_b200/libocpgpu.so")
 buf = (ctypes.c_ulonglong * 16)()
 lib.ocp_debug_phase(buf)
 v = np.array(list(buf), dtype=float)[8:]
-names = ["", "store + E", "P2 row block", "P3a trailing", "P3b column block", "P1 pivot inverse",
-         "P1 subnormal entries (exp)", "P1 entries < 1e-250 (exp)"]
-tot = v[1:6].sum()
+names = ["", "E2", "P2 row block", "P3a trailing", "P3b column block", "P1 pivot inverse",
+         "store (TMA issue + wait read)", "E1 scale"]
+tot = v[1:8].sum()
 
 for k in range(1, 8):
     print(f"{names[k]:28s} {100 * v[k] / tot:5.1f}%  {v[k]:.3e} cycles")
