@@ -151,6 +151,17 @@ def _probe(name, key):
         return None
 
 
+def load_traffic():
+    """DRAM bytes per launch of the hot kernels from the committed ncu --set full
+    captures (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
 def measure_fp64_peak():
     """FP64 roof: the larger of the DMMA (tensor) and DFMA probes measured in this run.
 
@@ -272,12 +283,12 @@ def run_ours(args):
                                    "launches": st["resid_launches"], "avg_ms": res_avg_ms,
                                    "share_of_step": st["resid_ms"] / ms_total,
                                    "algorithmic_bytes_per_launch": res_bytes},
-        "band_factor": {"bound": "fp64", "achieved": fac_tf, "peak": fp64_tf, "unit": "TFLOP/s",
+        "block_factor": {"bound": "fp64", "achieved": fac_tf, "peak": fp64_tf, "unit": "TFLOP/s",
                         "frac": (fac_tf / fp64_tf) if fac_tf and fp64_tf else None,
                         "peak_source": fp64_src, "launches": st["factor_launches"],
                         "avg_ms": fac_avg_ms, "share_of_step": st["factor_ms"] / ms_total,
                         "algorithmic_flops_per_launch": fac_flops},
-        "jvp_band_solve": {"bound": "hbm", "achieved": sol_gbs, "peak": hbm, "unit": "GB/s",
+        "jvp_block_solve": {"bound": "hbm", "achieved": sol_gbs, "peak": hbm, "unit": "GB/s",
                            "frac": (sol_gbs / hbm) if sol_gbs and hbm else None,
                            "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
                            "launches": st["solve_launches"], "avg_ms": sol_avg_ms,
@@ -286,8 +297,12 @@ def run_ours(args):
     }
     dominant = max(kernels, key=lambda k: kernels[k]["share_of_step"] or 0.0)
     kd = kernels[dominant]
+    traffic = load_traffic().get(dominant)
     roofline = {"kernel": dominant, "bound": kd["bound"], "achieved": kd["achieved"],
-                "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"], "traffic": None}
+                "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"],
+                "traffic": traffic["bytes_per_launch"] if traffic else None}
+    if traffic:
+        roofline["traffic_source"] = traffic["source"]
 
     cpu = None
     if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:

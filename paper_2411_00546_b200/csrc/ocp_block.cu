@@ -104,8 +104,8 @@ __device__ __forceinline__ double rcp64(double x) {
 // from one of two ping-pong 32x33 buffers and writes its updated entries to
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
-constexpr int PW = 8;   // all warps of the CTA
 constexpr int WLD = 33;
+template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
   constexpr int R = 32 / PW;
@@ -320,17 +320,17 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     }
     __syncthreads();
     BPH_MARK(1);
-    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels; every
-    //      phase runs on all warps (the latency-bound pivot chain slows down
-    //      next to concurrent DMMA traffic)
+    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels.  P1 of
+    //      panel 0 runs on all warps; P1 of panel p+1 runs on warps 0..3
+    //      (lookahead) as soon as they have updated the next pivot block,
+    //      concurrently with the other trailing tiles on warps 4..7.
+    pivot_inverse32<8>(R.row(0), lds, W0, W1, warp, lane, bad);
+    __syncthreads();
+    BPH_MARK(5);
     for (int p = 0; p < npan; ++p) {
       const int p0 = 32 * p;
       double* Prow = R.row(p0);                 // the pivot row block
       const double* Pinv = Prow + p0;
-      // ---- P1: Pinv = inverse of the pivot block
-      pivot_inverse32(Prow + p0, lds, W0, W1, warp, lane, bad);
-      __syncthreads();
-      BPH_MARK(5);
       // ---- P2: row block S[p, j] = Pinv S[p, j] (column tiles of 16 outside p)
       for (int tI = warp; tI < nct - 2; tI += NW) {
         const int j0 = 16 * (tI + (tI >= 2 * p ? 2 : 0));
@@ -343,7 +343,8 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       // ---- P3a: S[i, j] -= S[i, p] S[p, j]   (i, j outside p)
       {
         const int ncw = nct - 2, total = (npan - 1) * ncw;
-        for (int tI = warp; tI < total; tI += NW) {
+        const bool la = p + 1 < npan;
+        auto tile = [&](int tI) {
           int rt = tI / ncw, ct = tI - rt * ncw;
           rt += rt >= p ? 1 : 0;
           ct += ct >= 2 * p ? 2 : 0;
@@ -352,6 +353,21 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           load_c(Ci + 16 * ct, lds, c, lane);
           tile_32x16(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
           store_c(Ci + 16 * ct, lds, c, lane);
+        };
+        if (!la) {
+          for (int tI = warp; tI < total; tI += NW) tile(tI);
+        } else {
+          // the two tiles of the next pivot block: row tile p+1 is tile row p
+          // of the compressed numbering, its column tiles 2p+2, 2p+3 -> 2p, 2p+1
+          const int la0 = p * ncw + 2 * p;
+          if (warp < 4) {
+            if (warp < 2) tile(la0 + warp);
+            asm volatile("bar.sync 2, %0;" ::"n"(128) : "memory");
+            pivot_inverse32<4>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, bad);
+          } else {
+            for (int tI = warp - 4; tI < total; tI += 4)
+              if (tI != la0 && tI != la0 + 1) tile(tI);
+          }
         }
       }
       __syncthreads();

@@ -71,7 +71,7 @@ k_arnoldi(long long n, const double* __restrict__ Q, long long ldq, int j,
     if (threadIdx.x == 0) part[blockIdx.x] = bsum;
     grid.sync();
     double v = 0.0;
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) v += part[b];
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) v += __ldcg(part + b);
     const double h = block_sum_all<ARN_THREADS>(v, red);
     if (norm_pass) {
       const double hn = sqrt(h);
@@ -154,7 +154,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     if (tid == 0) part[blockIdx.x] = bsum;
     grid.sync();
     double v = 0.0;
-    for (int b = tid; b < nb; b += blockDim.x) v += part[b];
+    for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
     const double h = block_sum_all<ARN_THREADS>(v, red);
     if (norm_pass) {
       const double hn = sqrt(h);
