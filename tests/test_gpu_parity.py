@@ -329,3 +329,30 @@ def test_fused_native_gmres_matches_python_gmres():
     assert r1.converged and r2.converged and r1.iters == r2.iters
     np.testing.assert_allclose(r2.history, r1.history, rtol=1e-10)
     assert rel_l2(r2.x.to_host(), r1.x.to_host()) <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_band_and_block_factor_formats_agree(name, monkeypatch):
+    """The two stored-factor formats of the native library - the banded LU
+    (OCP_FACTOR_FORMAT=band) and the default block-tridiagonal inverse
+    format - give the same solve: same iteration counts, same iterate to
+    round-off, both matching the reference fixture."""
+    g = golden(f"{name}_tol1e-08.npz")
+    cfg = CONFIGS[name]
+    spec = build_spec(cfg, with_matrix=False)
+    out = {}
+    for fmt in ("band", "block"):
+        monkeypatch.setenv("OCP_FACTOR_FORMAT", fmt)
+        dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)   # fresh engine per format
+        x, rep = raspen_solve(np.zeros(cfg.unknowns), dec, spec,
+                              ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min),
+                              cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+                              krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000), inner_tol=1e-8)
+        out[fmt] = (x, rep)
+    (xb, rb), (xk, rk) = out["band"], out["block"]
+    assert rb.outer_iters == rk.outer_iters == int(g["outer_iters"])
+    assert rb.inner_iters == rk.inner_iters
+    assert all(abs(a - b) <= 1 for a, b in zip(rb.gmres_iters, rk.gmres_iters))
+    assert rel_l2(xb, xk) <= 1e-10
+    n2 = cfg.n * cfg.n
+    assert rel_l2(xk[:n2], g["y"]) <= 1e-8
