@@ -21,7 +21,8 @@
 #include "ocp_kernels.cuh"
 
 using namespace ocp;
-namespace ocp { void read_phase(unsigned long long* out); void read_bphase(unsigned long long* out); }
+namespace ocp { void read_phase(unsigned long long* out); void read_bphase(unsigned long long* out);
+                void read_aphase(unsigned long long* out); }
 
 namespace {
 
@@ -1404,7 +1405,12 @@ int ocp_reset_stats(ocp_ctx* ctx) {
 }
 
 #ifdef OCP_PHASE_TIMING
-int ocp_debug_phase(unsigned long long* out) { ocp::read_phase(out); ocp::read_bphase(out + 8); return 0; }
+int ocp_debug_phase(unsigned long long* out) {
+  ocp::read_phase(out);
+  ocp::read_bphase(out + 8);
+  ocp::read_aphase(out + 16);
+  return 0;
+}
 #endif
 
 int ocp_event_record(ocp_ctx* ctx, int slot) {

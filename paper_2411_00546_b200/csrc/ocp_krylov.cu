@@ -131,6 +131,14 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     const bool norm_pass = (i == j + 1);
     const double* cur = qb + (i & 1) * per;
     double acc = 0.0;
+    // q_{i+1} goes into the buffer of q_{i-1} as soon as every thread is done
+    // with pass i-1's axpy: the HBM stream then runs under this whole pass
+    __syncthreads();
+    if (tid == 0 && i + 1 <= j && cnt > 0) {
+      uint64_t* bar = &bars[(i + 1) & 1];
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(qb + ((i + 1) & 1) * per, Q + (long long)(i + 1) * ldq + b0, bytes, bar);
+    }
     if (!norm_pass) {
       if (cnt > 0) mbar_wait(&bars[i & 1], (i >> 1) & 1);
 #pragma unroll
@@ -142,14 +150,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
 #pragma unroll
       for (int k = 0; k < CH; ++k) acc = fma(w[k], w[k], acc);
     }
-    // (the barrier inside block_sum_all also retires every read of the other
-    //  buffer from pass i-1, so it can be refilled now)
     const double bsum = block_sum_all<ARN_THREADS>(acc, red);
-    if (tid == 0 && i + 1 <= j && cnt > 0) {
-      uint64_t* bar = &bars[(i + 1) & 1];
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(qb + ((i + 1) & 1) * per, Q + (long long)(i + 1) * ldq + b0, bytes, bar);
-    }
     double* part = partials + (i & 1) * nb;
     if (tid == 0) part[blockIdx.x] = bsum;
     grid.sync();
