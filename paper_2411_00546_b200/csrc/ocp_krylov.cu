@@ -139,12 +139,14 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
       mbar_expect_tx(bar, bytes);
       bulk_g2s(qb + ((i + 1) & 1) * per, Q + (long long)(i + 1) * ldq + b0, bytes, bar);
     }
+    double qv[CH];   // q_i stays in registers for the axpy (one shared-memory read)
     if (!norm_pass) {
       if (cnt > 0) mbar_wait(&bars[i & 1], (i >> 1) & 1);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int e = tid + k * ARN_THREADS;
-        acc = fma(e < cnt ? cur[e] : 0.0, w[k], acc);
+        qv[k] = e < cnt ? cur[e] : 0.0;
+        acc = fma(qv[k], w[k], acc);
       }
     } else {
 #pragma unroll
@@ -169,10 +171,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     } else {
       if (blockIdx.x == 0 && tid == 0) h_out[i] = h;
 #pragma unroll
-      for (int k = 0; k < CH; ++k) {
-        const int e = tid + k * ARN_THREADS;
-        w[k] = __dsub_rn(w[k], __dmul_rn(h, e < cnt ? cur[e] : 0.0));
-      }
+      for (int k = 0; k < CH; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, qv[k]));
     }
   }
 }
@@ -214,6 +213,7 @@ cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const doub
       if (per <= 8 * ARN_THREADS) e = launch_db<8>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
       else if (per <= 16 * ARN_THREADS) e = launch_db<16>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
       else if (per <= 24 * ARN_THREADS) e = launch_db<24>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      else if (per <= 28 * ARN_THREADS) e = launch_db<28>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
       else e = launch_db<32>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
       if (e != cudaErrorNotSupported) return e;
       cudaGetLastError();
