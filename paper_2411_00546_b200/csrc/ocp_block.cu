@@ -105,6 +105,7 @@ __device__ __forceinline__ double rcp64(double x) {
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
 constexpr int WLD = 33;
+constexpr int LAW = 2;   // lookahead warps: the next pivot inverse while the others update
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
@@ -360,12 +361,12 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           // the two tiles of the next pivot block: row tile p+1 is tile row p
           // of the compressed numbering, its column tiles 2p+2, 2p+3 -> 2p, 2p+1
           const int la0 = p * ncw + 2 * p;
-          if (warp < 4) {
-            if (warp < 2) tile(la0 + warp);
-            asm volatile("bar.sync 2, %0;" ::"n"(128) : "memory");
-            pivot_inverse32<4>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, bad);
+          if (warp < LAW) {
+            for (int t2 = warp; t2 < 2; t2 += LAW) tile(la0 + t2);   // the two lookahead tiles
+            asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
+            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, bad);
           } else {
-            for (int tI = warp - 4; tI < total; tI += 4)
+            for (int tI = warp - LAW; tI < total; tI += NW - LAW)
               if (tI != la0 && tI != la0 + 1) tile(tI);
           }
         }
