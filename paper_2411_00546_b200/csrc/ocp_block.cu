@@ -109,6 +109,10 @@ constexpr int LAW = 2;   // lookahead warps: the next pivot inverse while the ot
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
+  // Gauss-Jordan with 2x2 pivot blocks: 16 dependent steps instead of 32.
+  // Step s eliminates rows/columns K = {k, k+1}, k = 2s:
+  //   S[K,K] <- P^{-1};  S[K,j] <- P^{-1} S[K,j];  S[i,K] <- -S[i,K] P^{-1};
+  //   S[i,j] <- S[i,j] - S[i,K] (P^{-1} S[K,j])
   constexpr int R = 32 / PW;
   double c[R];
 #pragma unroll
@@ -119,41 +123,43 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   bool ok = true;
 #pragma unroll 1
-  for (int k = 0; k < 32; ++k) {
-    const double* Wr = (k & 1) ? W1 : W0;
-    double* Ww = (k & 1) ? W0 : W1;
-    const double piv = Wr[k * WLD + k];
-    const double ck = Wr[k * WLD + lane];
-    double f[R];
+  for (int k = 0; k < 32; k += 2) {
+    const double* Wr = (k & 2) ? W1 : W0;
+    double* Ww = (k & 2) ? W0 : W1;
+    const double p00 = Wr[k * WLD + k], p01 = Wr[k * WLD + k + 1];
+    const double p10 = Wr[(k + 1) * WLD + k], p11 = Wr[(k + 1) * WLD + k + 1];
+    const double b0 = Wr[k * WLD + lane], b1 = Wr[(k + 1) * WLD + lane];   // S[K, lane]
+    double f0[R], f1[R];
 #pragma unroll
-    for (int i = 0; i < R; ++i) f[i] = Wr[(R * wsub + i) * WLD + k];
-    ok = ok && piv != 0.0 && isfinite(piv);
-    const double rp = rcp64(piv);
-    const bool me = lane == k;
-    const double m = me ? rp : ck * rp;   // the new row-k entry of this column
+    for (int i = 0; i < R; ++i) {
+      f0[i] = Wr[(R * wsub + i) * WLD + k];
+      f1[i] = Wr[(R * wsub + i) * WLD + k + 1];
+    }
+    const double det = fma(p00, p11, -p01 * p10);
+    ok = ok && det != 0.0 && isfinite(det);
+    const double rd = rcp64(det);
+    const double q00 = p11 * rd, q01 = -p01 * rd, q10 = -p10 * rd, q11 = p00 * rd;   // P^{-1}
+    const int t = lane - k;                        // 0 / 1: this column is in K
+    const bool inK = t == 0 || t == 1;
+    // new S[K, lane]: P^{-1} column t for lanes in K, P^{-1} S[K, lane] otherwise
+    const double m0 = inK ? (t == 0 ? q00 : q01) : fma(q00, b0, q01 * b1);
+    const double m1 = inK ? (t == 0 ? q10 : q11) : fma(q10, b0, q11 * b1);
 #pragma unroll
     for (int i = 0; i < R; ++i) {
       const int row = R * wsub + i;
-      c[i] = row == k ? m : fma(-f[i], m, me ? 0.0 : c[i]);
-      Ww[row * WLD + lane] = c[i];
+      double v;
+      if (row == k) v = m0;
+      else if (row == k + 1) v = m1;
+      else v = fma(-f0[i], m0, fma(-f1[i], m1, inK ? 0.0 : c[i]));
+      c[i] = v;
+      // publish what the next step reads: its pivot rows and columns
+      if (row == k + 2 || row == k + 3 || lane == k + 2 || lane == k + 3) Ww[row * WLD + lane] = v;
     }
     asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
   if (!ok) *bad = 1;
-#ifdef OCP_EXP_COUNT_SUB
-  {
-    int sub = 0, tiny = 0;
-    for (int i = 0; i < R; ++i) {
-      const double v = fabs(c[i]);
-      sub += (v != 0.0 && v < 2.2250738585072014e-308);
-      tiny += (v != 0.0 && v < 1e-250);
-    }
-    if (sub) atomicAdd(&g_bphase[6], (unsigned long long)sub);
-    if (tiny) atomicAdd(&g_bphase[7], (unsigned long long)tiny);
-  }
-#endif
 }
 
 // one 32x16 DMMA tile: C (+)= sgn * A[32 x 32] * B[32 x 16]

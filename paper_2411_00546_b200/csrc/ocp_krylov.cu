@@ -39,6 +39,26 @@ __device__ __forceinline__ double block_sum_all(double v, double* red) {
 
 constexpr int ARN_THREADS = 512;
 
+// optional per-phase cycle counters of block 0 (build with -DOCP_PHASE_TIMING; tools/aphase_dbg.py)
+#ifdef OCP_PHASE_TIMING
+__device__ unsigned long long g_aphase[8];
+void read_aphase(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, g_aphase, 8 * sizeof(unsigned long long));
+}
+#define APH_START() long long t_last = clock64()
+#define APH(k)                                                                          \
+  do {                                                                                  \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                          \
+      const long long now = clock64();                                                  \
+      atomicAdd(&g_aphase[k], (unsigned long long)(now - t_last));                      \
+      t_last = now;                                                                     \
+    }                                                                                   \
+  } while (0)
+#else
+#define APH_START() (void)0
+#define APH(k) (void)0
+#endif
+
 template <int CH>
 __global__ void __launch_bounds__(ARN_THREADS, 1)
 k_arnoldi(long long n, const double* __restrict__ Q, long long ldq, int j,
@@ -127,6 +147,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     bulk_g2s(qb, Q + b0, bytes, &bars[0]);
   }
   const int nb = gridDim.x;
+  APH_START();
   for (int i = 0; i <= j + 1; ++i) {
     const bool norm_pass = (i == j + 1);
     const double* cur = qb + (i & 1) * per;
@@ -142,6 +163,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     double qv[CH];   // q_i stays in registers for the axpy (one shared-memory read)
     if (!norm_pass) {
       if (cnt > 0) mbar_wait(&bars[i & 1], (i >> 1) & 1);
+      APH(0);
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int e = tid + k * ARN_THREADS;
@@ -155,10 +177,13 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     const double bsum = block_sum_all<ARN_THREADS>(acc, red);
     double* part = partials + (i & 1) * nb;
     if (tid == 0) part[blockIdx.x] = bsum;
+    APH(1);
     grid.sync();
+    APH(2);
     double v = 0.0;
     for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
     const double h = block_sum_all<ARN_THREADS>(v, red);
+    APH(3);
     if (norm_pass) {
       const double hn = sqrt(h);
       if (blockIdx.x == 0 && tid == 0) h_out[i] = hn;
@@ -173,6 +198,7 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
 #pragma unroll
       for (int k = 0; k < CH; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, qv[k]));
     }
+    APH(4);
   }
 }
 
