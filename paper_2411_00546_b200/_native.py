@@ -11,7 +11,7 @@ import threading
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libocpgpu.so")
+LIB_PATH = os.environ.get("OCP_LIB") or os.path.join(HERE, "libocpgpu.so")   # OCP_LIB: experiment builds
 
 OCP_OK = 0
 OCP_ERR_ARG = 1

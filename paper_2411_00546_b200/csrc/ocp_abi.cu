@@ -389,9 +389,10 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
         const double kstop = 2.0 * s.nc * a_own;
         ctx->sub_jbytes.push_back(8.0 * ((double)s.N * s.w + ((double)s.N - kstop) * (s.w + 1.0)));
       } else {
-        // S_a^{-1} per line: forward reads all nr, backward nr-1-a_stop of them
-        const double blk = 8.0 * (double)s.NPS * s.NPS;
-        fac += (long long)s.nr * s.NPS * s.NPS;
+        // the upper 16-tile triangle of W_a = S_a^{-1} P per line (block_line_doubles):
+        // forward reads all nr, backward nr-1-a_stop of them
+        const double blk = 8.0 * (double)block_line_doubles(s.NPS);
+        fac += (long long)s.nr * block_line_doubles(s.NPS);
         ctx->sub_fbytes.push_back(blk * (2.0 * s.nr - 1.0));
         ctx->sub_jbytes.push_back(blk * (s.nr + std::max(0, s.nr - 1 - a_own)));
       }

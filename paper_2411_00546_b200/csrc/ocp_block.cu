@@ -10,12 +10,16 @@
 // and a solve is
 //     forward   w_a = S_a^{-1} (r_a - off w_{a-1})
 //     backward  x_a = w_a - off S_a^{-1} x_{a+1}.
-// The factor store keeps every S_a^{-1} (n x n, padded to NPS = round16(n),
-// identity on the padding) in COLUMN-major order: half the bytes of the band
-// factors, the same bytes per solve, and the solve becomes dense mat-vecs in
-// which every thread owns one output row (no reductions).  The factor runs
-// the recursion on the transposes, S_a^T = D_a^T - off^2 (S_{a-1}^{-1})^T, so
-// its row-major result is already the column-major S_a^{-1}.
+// P J is symmetric (P swaps the y / p unknowns of every point: J = [[K, B12],
+// [B21, K]] with K = A + diag(phi') symmetric and B12, B21 diagonal), so
+// J^T = P J P, every Schur complement keeps S_a^T = P S_a P, and
+// W_a = S_a^{-1} P is symmetric.  The factor store keeps, per line, only the
+// upper triangle of 16x16 tiles of W_a (NPS = round16(n), identity on the
+// padding), tile column by tile column, each column-major: 55 of 100 tiles at
+// NPS = 160, so a solve streams 55 % of the bytes of the full inverse.  The
+// factor runs the recursion on the transposes, S_a^T = D_a^T - off^2
+// (S_{a-1}^{-1})^T, so shared row i of its result is column i of S_a^{-1},
+// and column j of W_a is the head of shared row j^1.
 //
 // k_block_factor: one CTA per subdomain; S stays resident in shared memory
 // (NPB <= 160; larger blocks use a per-CTA global scratch, L2-resident) and is
@@ -28,10 +32,11 @@
 // the 32x32 pivot inverses is a DMMA (mma.sync.m8n8k4.f64) on shared-memory
 // operands; nothing round-trips through L2 (the band kernel's bottleneck).
 //
-// k_block_solve<MODE>: one CTA per subdomain; S_a^{-1} streams through a ring
-// of TMA bulk-copy stages in chunks of 16 columns; thread t accumulates
-// output row t; MODE 1 (JVP / RAS apply) stops the backward sweep at the
-// first owned line (schwarz.py:344).
+// k_block_solve<MODE>: one CTA per subdomain; the tile columns of W_a stream
+// through a ring of TMA bulk-copy stages; thread t accumulates output row t
+// from the stored tiles and every off-diagonal tile is applied a second time,
+// transposed, by 16-lane column reductions; MODE 1 (JVP / RAS apply) stops
+// the backward sweep at the first owned line (schwarz.py:344).
 #include "ocp_kernels.cuh"
 #include "ocp_tma.cuh"
 
@@ -57,8 +62,13 @@ void read_bphase(unsigned long long* out) {
 #define BPH_START() (void)0
 #define BPH_MARK(k) (void)0
 #endif
-constexpr int BS_ROWS = 16;      // rows per solve chunk
 constexpr int BS_STAGES = 4;     // TMA ring depth of the solve
+#ifndef OCP_BS_PF_EARLY
+#define OCP_BS_PF_EARLY 0
+#endif
+// the solve prefetches line a+1 into L2 at stage nst-1-BS_PF_EARLY of line a (< 0: off)
+constexpr int BS_PF_EARLY = OCP_BS_PF_EARLY;
+constexpr int BS_MAX_THREADS = 480;   // 2 threads per row + a producer warp, NPS <= 224
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -250,26 +260,35 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
   const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr, lds = R.lds;
   const int npan = NPB / 32, nct = NPB / 16;
   const double mo2 = -(off * off);
-  const long long bsz = (long long)NPS * NPS;   // stored block (rows/cols >= n are identity/zero)
+  const long long lsz = block_line_doubles(NPS);   // stored doubles per line
   BPH_START();
   // the Jacobian diagonals of the next line are loaded one line ahead
   // (registers) and staged in shared memory (JL) at the start of its E phase
   const int nq = 4 * s.nc;
   double jn0 = tid < nq ? JD[tid] : 0.0, jn1 = tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
-  // S^{-1} of a line goes to the factor store by TMA bulk stores (one per
-  // shared row, issued by warp 0): the copies run on the TMA engine, so no
-  // global store traffic sits in the load/store queues of the compute phases
+  // W = S^{-1} P of a line goes to the factor store by TMA bulk stores (issued
+  // by warp 0): the copies run on the TMA engine, so no global store traffic
+  // sits in the load/store queues of the compute phases.  Shared row i holds
+  // column i of S^{-1}, so column j of W (rows 0 .. 16c+15 of the upper tile
+  // triangle, c = j / 16) is the head of shared row j^1: one copy per column.
   auto store_block = [&](int line) {
-    double* dst = fac + (long long)line * bsz;
+    double* dst = fac + (long long)line * lsz;
     const int rs = SPLIT ? (R.r0 < NPS ? R.r0 : NPS) : NPS;   // rows held in shared memory
+    const int cpb = NPS / 16;
+    auto col_off = [cpb](int j) {
+      const int c = j >> 4;
+      return block_col_off(c, cpb) + (long long)(j - 16 * c) * (16 * c + 18);
+    };
     if (warp == 0) {
-      for (int i = lane; i < rs; i += 32)
-        bulk_s2g(dst + (long long)i * NPS, R.row(i), (uint32_t)(NPS * sizeof(double)));
+      for (int j = lane; j < rs; j += 32)
+        bulk_s2g(dst + col_off(j), R.row(j ^ 1), (uint32_t)((16 * (j >> 4) + 16) * sizeof(double)));
       bulk_commit();
     }
     if (SPLIT)
-      for (int i = rs + warp; i < NPS; i += NW)
-        for (int j = lane; j < NPS; j += 32) __stcs(dst + (long long)i * NPS + j, R.row(i)[j]);
+      for (int j = rs + warp; j < NPS; j += NW) {
+        const int m16 = 16 * (j >> 4) + 16;
+        for (int r = lane; r < m16; r += 32) __stcs(dst + col_off(j) + r, R.row(j ^ 1)[r]);
+      }
     if (warp == 0) bulk_wait_read();
     __syncthreads();
   };
@@ -443,108 +462,179 @@ int block_factor_smem_bytes(int max_npb) {
 // ---------------------------------------------------------------------------
 // solve with the stored S_a^{-1}
 // ---------------------------------------------------------------------------
+// One stage of the solve ring holds two tile columns of a line, c and
+// cpb-1-c (the middle one alone when cpb is odd), so every stage carries the
+// same bytes (~90 KB in flight per CTA).  Stages are sized for pairs up to
+// cpb = 10 (two CTAs per SM); a subdomain whose pairs do not fit streams one
+// tile column per stage.
+__host__ __device__ inline int bs_stage_doubles(int max_nps) {
+  const int cpb = max_nps / 16, pc = cpb < 10 ? cpb : 10;
+  const int pair = 256 * pc + 320, single = (int)block_col_doubles(cpb - 1);
+  return pair > single ? pair : single;
+}
+// two threads per row (one warp per tile row) + one producer warp
+__host__ __device__ inline int bs_threads(int max_nps) { return 2 * max_nps + 32; }
+
+// Solve with the stored W_a.  Thread (i, h) (warp ti = i / 16, lane = 16h +
+// i % 16) accumulates two halves of row i of the FULL symmetric W_a v':
+//   row part     W[i][16c + 8h + k] v'[16c + 8h + k]   stored tiles (ti, c), c >= ti
+//   column part  W[r][i] v'[r], r < 16 ti, r = 4q + 2h + {0, 1}  (= W[i][r])
+// so every thread does 8 cpb FMAs per line whatever its tile, no cross-thread
+// reductions are needed (one shuffle joins the halves), and each stored
+// element is read from shared memory twice (once per product).  Warps move
+// through the ring independently: a producer warp refills a slot once every
+// consumer warp has released it (empty mbarriers), and the consumers meet
+// once per line (named barrier 1) because line a+1 needs all of line a.
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(BS_MAX_THREADS, 2)
 k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
               double scale, double* out_pool, double off, int max_npb) {
   extern __shared__ __align__(16) double sm[];
   const SubInfo s = subs[list[blockIdx.x]];
-  const int tid = threadIdx.x;
-  const int NPB = s.NPS, n = 2 * s.nc, nr = s.nr;   // stored block size (multiple of 16)
-  const int SB = BS_ROWS * NPB;                       // doubles per stage
-  double* stage = sm;                                 // [BS_STAGES][BS_ROWS][NPB]
-  double* vin = sm + BS_STAGES * BS_ROWS * max_npb;   // mat-vec input of the current line
-  __shared__ __align__(8) uint64_t bars[BS_STAGES];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NPS = s.NPS, n = 2 * s.nc, nr = s.nr;   // stored block size (multiple of 16)
+  const int SBS = bs_stage_doubles(max_npb);
+  double* stage = sm;                                 // [BS_STAGES][SBS]
+  double* vp = sm + BS_STAGES * SBS;                  // [2][max_npb]: P vin, double-buffered by line
+  __shared__ __align__(8) uint64_t full[BS_STAGES], empty[BS_STAGES];
   const double* fac = fac_pool + s.fac;
   const double* in = in_pool + s.loc;
   double* out = out_pool + s.loc;
-  const long long bsz = (long long)NPB * NPB;
-  const int cpb = NPB / BS_ROWS;                      // chunks per line
+  const long long lsz = block_line_doubles(NPS);
+  const int cpb = NPS / 16;                           // tile columns per line = consumer warps
+  const bool paired = 256 * cpb + 320 <= SBS;
+  const int nst = paired ? (cpb + 1) / 2 : cpb;       // stages per line
   int a_stop = 0;
   if (MODE == 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
   const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;   // lines a = nr-2 .. a_stop
-  const int total = (nr + nback) * cpb;
-  auto chunk_src = [&](int t) -> const double* {
-    const int blk = t / cpb, c = t - blk * cpb;
-    const int a = blk < nr ? blk : nr - 2 - (blk - nr);
-    return fac + a * bsz + (long long)c * SB;
-  };
-  const uint32_t bytes = (uint32_t)(SB * sizeof(double));
+  const int nlines = nr + nback, total = nlines * nst;
   if (tid == 0) {
-    for (int i = 0; i < BS_STAGES; ++i) mbar_init(&bars[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int t = 0; t < BS_STAGES && t < total; ++t) {
-      mbar_expect_tx(&bars[t], bytes);
-      bulk_g2s(stage + t * SB, chunk_src(t), bytes, &bars[t]);
+    for (int i = 0; i < BS_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], cpb);
     }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // line 0 input
-  for (int t = tid; t < NPB; t += blockDim.x) vin[t] = t < n ? scale * in[t] : 0.0;
+  // line 0 input, stored permuted: vp[t ^ 1] = vin[t]
+  for (int t = tid; t < NPS; t += blockDim.x) vp[t ^ 1] = t < n ? scale * in[t] : 0.0;
   __syncthreads();
-  int t = 0;
-  // thread `tid` owns output row tid of every line (tid < NPB)
-  for (int blk = 0; blk < nr + nback; ++blk) {
+  if (warp == (int)(blockDim.x >> 5) - 1) {
+    // ---- producer: stage t = (line blk, k) into slot t % BS_STAGES
+    if (lane == 0) {
+      // the next line is prefetched into L2 as one bulk range while the
+      // ring issues the last BS_PF_EARLY+1 stages of the current line
+      auto line_of = [&](int b) { return b < nr ? b : nr - 2 - (b - nr); };
+      const int kpf = nst - 1 - BS_PF_EARLY > 0 ? nst - 1 - BS_PF_EARLY : 0;
+      int blk = 0, k = 0;
+      for (int t = 0; t < total; ++t) {
+        const int st = t % BS_STAGES;
+        if (t >= BS_STAGES) mbar_wait(&empty[st], ((t / BS_STAGES) - 1) & 1);
+        const int a = line_of(blk);
+        const int k2 = paired ? cpb - 1 - k : k;
+        const double* src = fac + a * lsz;
+        // a pair (k, cpb-1-k) is contiguous in the store
+        const uint32_t bytes = (uint32_t)(8 * (block_col_doubles(k) + (k2 != k ? block_col_doubles(k2) : 0)));
+        mbar_expect_tx(&full[st], bytes);
+        // (one copy per tile column measured ~1 % faster than one per pair)
+        bulk_g2s(stage + st * SBS, src + block_col_off(k, cpb), (uint32_t)(8 * block_col_doubles(k)),
+                 &full[st]);
+        if (k2 != k)
+          bulk_g2s(stage + st * SBS + block_col_doubles(k), src + block_col_off(k2, cpb),
+                   (uint32_t)(8 * block_col_doubles(k2)), &full[st]);
+        if (BS_PF_EARLY >= 0 && k == kpf && blk + 1 < nlines)
+          bulk_prefetch_l2(fac + line_of(blk + 1) * lsz, (uint32_t)(8 * lsz));
+        if (++k == nst) { k = 0; ++blk; }
+      }
+    }
+    return;
+  }
+  if (warp >= cpb) return;   // consumer warps beyond this subdomain's tile rows
+  const int ti = warp, jj = lane & 15, h = lane >> 4, i = 16 * ti + jj;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int blk = 0; blk < nlines; ++blk) {
     const bool fwd = blk < nr;
     const int a = fwd ? blk : nr - 2 - (blk - nr);
-    // prefetch of this thread's combine operand (in_{a+1} forward, w_a backward)
+    const double* v = vp + (blk & 1) * max_npb;
+    double* vnext = vp + ((blk + 1) & 1) * max_npb;
+    // prefetch of this row's combine operand (in_{a+1} forward, w_a backward)
     double nxt = 0.0;
-    if (tid < n) {
+    if (h == 0 && i < n) {
       if (fwd) {
-        if (a + 1 < nr) nxt = in[(long long)(a + 1) * n + tid];
+        if (a + 1 < nr) nxt = in[(long long)(a + 1) * n + i];
       } else {
-        nxt = out[(long long)a * n + tid];
+        nxt = out[(long long)a * n + i];
       }
     }
-    double y0 = 0.0, y1 = 0.0;
-    for (int c = 0; c < cpb; ++c, ++t) {
-      const int st = t % BS_STAGES;
-      mbar_wait(&bars[st], (t / BS_STAGES) & 1);
-      const double* ch = stage + st * SB;   // columns c*16 .. c*16+15 of S_a^{-1}
-      if (tid < NPB) {
-        const double* vc = vin + c * BS_ROWS;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    auto tile_column = [&](const double* cb, int c) {
+      const int ld2 = 16 * c + 18;
+      if (c >= ti) {   // row part: this row's 8 columns of tile (ti, c)
+        const double* w = cb + 8 * h * ld2 + i;
+        const double2* vv = reinterpret_cast<const double2*>(v + 16 * c + 8 * h);
 #pragma unroll
-        for (int cc = 0; cc < BS_ROWS; cc += 2) {
-          y0 = fma(ch[cc * NPB + tid], vc[cc], y0);
-          y1 = fma(ch[(cc + 1) * NPB + tid], vc[cc + 1], y1);
+        for (int k = 0; k < 8; k += 2) {
+          const double2 x = vv[k >> 1];
+          p0 = fma(w[k * ld2], x.x, p0);
+          p1 = fma(w[(k + 1) * ld2], x.y, p1);
         }
       }
-      __syncthreads();
-      if (tid == 0 && t + BS_STAGES < total) {
-        mbar_expect_tx(&bars[st], bytes);
-        bulk_g2s(stage + st * SB, chunk_src(t + BS_STAGES), bytes, &bars[st]);
+      if (c == ti) {   // column part: stored column i above the diagonal tile
+        const double* cj = cb + jj * ld2 + 2 * h;
+        const double* vr = v + 2 * h;
+#pragma unroll 4
+        for (int r = 0; r < 16 * c; r += 4) {
+          const double2 x = *reinterpret_cast<const double2*>(cj + r);
+          const double2 y = *reinterpret_cast<const double2*>(vr + r);
+          p2 = fma(x.x, y.x, p2);
+          p3 = fma(x.y, y.y, p3);
+        }
       }
+    };
+    for (int k = 0; k < nst; ++k) {
+      const int k2 = paired ? cpb - 1 - k : k;
+      mbar_wait(&full[st], ph);
+      const double* ch = stage + st * SBS;
+      tile_column(ch, k);
+      if (k2 != k) tile_column(ch + block_col_doubles(k), k2);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == BS_STAGES) { st = 0; ph ^= 1; }
     }
-    const double y = y0 + y1;   // (S_a^{-1} vin)[tid]
-    if (tid < NPB) {
+    double y = (p0 + p1) + (p2 + p3);
+    y += __shfl_xor_sync(0xffffffffu, y, 16);   // (S_a^{-1} vin)[i]
+    if (h == 0) {
       if (fwd) {
         // w_a = y; next input = scale in_{a+1} - off w_a (the last line starts
         // the backward sweep with x_{nr-1} = w_{nr-1})
-        const double w = tid < n ? y : 0.0;
-        if (tid < n) out[(long long)a * n + tid] = w;
-        vin[tid] = (a + 1 < nr) ? (tid < n ? fma(-off, w, scale * nxt) : 0.0) : w;
+        const double w = i < n ? y : 0.0;
+        if (i < n) out[(long long)a * n + i] = w;
+        vnext[i ^ 1] = (a + 1 < nr) ? (i < n ? fma(-off, w, scale * nxt) : 0.0) : w;
       } else {
         // x_a = w_a - off y ; next input = x_a
-        const double x = tid < n ? fma(-off, y, nxt) : 0.0;
-        if (tid < n) out[(long long)a * n + tid] = x;
-        vin[tid] = x;
+        const double x = i < n ? fma(-off, y, nxt) : 0.0;
+        if (i < n) out[(long long)a * n + i] = x;
+        vnext[i ^ 1] = x;
       }
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * cpb) : "memory");
   }
 }
 
 size_t block_solve_smem_bytes(int max_npb) {
-  return sizeof(double) * ((size_t)BS_STAGES * BS_ROWS * max_npb + 2 * (size_t)max_npb);
+  return sizeof(double) * ((size_t)BS_STAGES * bs_stage_doubles(max_npb) + 2 * (size_t)max_npb);
 }
 
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
                                const int* list, const double* fac, const double* in, double scale,
                                double* out_pool, double off, int max_npb) {
   const size_t smem = block_solve_smem_bytes(max_npb);
+  const int nt = bs_threads(max_npb);
+  if (nt > BS_MAX_THREADS) return cudaErrorInvalidConfiguration;
   if (mode == 0)
-    k_block_solve<0><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+    k_block_solve<0><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
   else
-    k_block_solve<1><<<grid, 256, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+    k_block_solve<1><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
   return cudaGetLastError();
 }
 

@@ -60,6 +60,23 @@ cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo
                               double* out_pool, int max_w);
 cudaError_t set_band_solve_smem(int bytes);
 // block-tridiagonal format (ocp_block.cu)
+// Per line the store keeps the upper triangle of 16x16 tiles of
+// W_a = S_a^{-1} P (P swaps the y / p unknowns of every point; W_a is
+// symmetric because P J is), by tile columns: tile column c holds columns
+// 16c .. 16c+15, rows 0 .. 16c+15, column-major with stride 16c+18 (two pad
+// doubles per column keep the transposed reads of the solve free of
+// shared-memory bank conflicts and every column 16-byte aligned).  The tile
+// columns are laid out in the order 0, cpb-1, 1, cpb-2, ...: the pair
+// (k, cpb-1-k) is one contiguous range of 256 cpb + 320 doubles, the unit
+// the solve streams.
+__host__ __device__ constexpr long long block_col_doubles(int c) { return 16LL * (16 * c + 18); }
+__host__ __device__ constexpr long long block_col_off(int c, int cpb) {
+  return (c < cpb - 1 - c ? c : cpb - 1 - c) * (256LL * cpb + 320) +
+         (c > cpb - 1 - c ? block_col_doubles(cpb - 1 - c) : 0LL);
+}
+__host__ __device__ constexpr long long block_line_doubles(int nps) {
+  return 128LL * (nps / 16) * (nps / 16) + 160LL * (nps / 16);
+}
 __global__ void k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
                                const double* JDpool, double* fac_pool, double* gscratch,
                                long long gs_stride, int* status);
