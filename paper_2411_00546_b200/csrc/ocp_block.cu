@@ -115,7 +115,10 @@ __device__ __forceinline__ double rcp64(double x) {
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
 constexpr int WLD = 33;
-constexpr int LAW = 2;   // lookahead warps: the next pivot inverse while the others update
+#ifndef OCP_LAW
+#define OCP_LAW 2
+#endif
+constexpr int LAW = OCP_LAW;   // lookahead warps: the next pivot inverse while the others update
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
@@ -259,18 +262,18 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
   constexpr int NW = BF_THREADS / 32;
   const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr, lds = R.lds;
   const int npan = NPB / 32, nct = NPB / 16;
-  const double mo2 = -(off * off);
+  const double off2 = off * off;
   const long long lsz = block_line_doubles(NPS);   // stored doubles per line
   BPH_START();
   // the Jacobian diagonals of the next line are loaded one line ahead
   // (registers) and staged in shared memory (JL) at the start of its E phase
   const int nq = 4 * s.nc;
   double jn0 = tid < nq ? JD[tid] : 0.0, jn1 = tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
-  // W = S^{-1} P of a line goes to the factor store by TMA bulk stores (issued
-  // by warp 0): the copies run on the TMA engine, so no global store traffic
-  // sits in the load/store queues of the compute phases.  Shared row i holds
-  // column i of S^{-1}, so column j of W (rows 0 .. 16c+15 of the upper tile
-  // triangle, c = j / 16) is the head of shared row j^1: one copy per column.
+  // -W of a line goes to the factor store by TMA bulk stores (issued by warp
+  // 0): the copies run on the TMA engine, so no global store traffic sits in
+  // the load/store queues of the compute phases.  The shared block is
+  // symmetric, so column j of the upper tile triangle (rows 0 .. 16c+15,
+  // c = j / 16) is the head of shared row j: one copy per column.
   auto store_block = [&](int line) {
     double* dst = fac + (long long)line * lsz;
     const int rs = SPLIT ? (R.r0 < NPS ? R.r0 : NPS) : NPS;   // rows held in shared memory
@@ -281,13 +284,13 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     };
     if (warp == 0) {
       for (int j = lane; j < rs; j += 32)
-        bulk_s2g(dst + col_off(j), R.row(j ^ 1), (uint32_t)((16 * (j >> 4) + 16) * sizeof(double)));
+        bulk_s2g(dst + col_off(j), R.row(j), (uint32_t)((16 * (j >> 4) + 16) * sizeof(double)));
       bulk_commit();
     }
     if (SPLIT)
       for (int j = rs + warp; j < NPS; j += NW) {
         const int m16 = 16 * (j >> 4) + 16;
-        for (int r = lane; r < m16; r += 32) __stcs(dst + col_off(j) + r, R.row(j ^ 1)[r]);
+        for (int r = lane; r < m16; r += 32) __stcs(dst + col_off(j) + r, R.row(j)[r]);
       }
     if (warp == 0) bulk_wait_read();
     __syncthreads();
@@ -303,9 +306,10 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     if (a > 0) store_block(a - 1);
     else __syncthreads();
     BPH_MARK(6);
-    // ---- E1. S = -off^2 S_{a-1}^{-1} on the real block, identity on the
-    //      padding (warp per row, double2 columns; all loads of a row pair are
-    //      issued before any store)
+    // ---- E1. M = -off^2 P W_{a-1} P = off^2 (-W_{a-1})[i^1][j^1] on the real
+    //      block (the shared block holds -W_{a-1}), identity on the padding
+    //      (warp per row pair, double2 columns; a pair's loads are issued
+    //      before its stores: new row i is old row i^1 with swapped columns)
     for (int i0 = 2 * warp; i0 < NPB; i0 += 2 * NW) {
       double2 v[2][4];
 #pragma unroll
@@ -326,8 +330,8 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           if (j >= NPB) continue;
           double2 w;
           if (i < n && j < n) {
-            w.x = mo2 * v[r][u].x;
-            w.y = mo2 * v[r][u].y;
+            w.x = off2 * v[1 - r][u].y;
+            w.y = off2 * v[1 - r][u].x;
           } else {
             w.x = i == j ? 1.0 : 0.0;
             w.y = i == j + 1 ? 1.0 : 0.0;
@@ -338,15 +342,21 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     }
     __syncthreads();
     BPH_MARK(7);
-    // ---- E2. + D_a^T: five diagonals of the real block (the recursion runs on
-    //      the transposes so that the stored inverse is column-major)
-    for (int e = tid; e < 5 * n; e += BF_THREADS) {
-      const int i = e / 5, j = i + (e - 5 * i) - 2;
-      if (j >= 0 && j < n) R.row(i)[j] += d_entry(s, JL, j, i, off);
+    // ---- E2. + P D_a: (P D_a)[i][j] = D_a[i^1][j], seven diagonals
+    for (int e = tid; e < 7 * n; e += BF_THREADS) {
+      const int i = e / 7, j = i + (e - 7 * i) - 3;
+      if (j >= 0 && j < n) R.row(i)[j] += d_entry(s, JL, i ^ 1, j, off);
     }
     __syncthreads();
     BPH_MARK(1);
-    // ---- Gauss-Jordan inversion of S in place, 32-wide pivot panels.  P1 of
+    // ---- Symmetric block sweep of M in place (Goodnight's sweep operator with
+    //      32-wide pivot panels: every intermediate stays symmetric and the
+    //      result is -M^{-1} = -W_a).  For pivot block A = M[p][p]:
+    //        P2   M[p][j] = A^{-1} M[p][j]            (row block, DMMA)
+    //        P3a  M[i][j] -= M[i][p] M[p][j]           upper 32x16 tiles only (DMMA);
+    //             strictly-upper tiles are mirrored into the lower triangle
+    //        P3b  M[i][p] = M[p][i]^T (transposed copy), M[p][p] = -A^{-1}
+    //      P1 of
     //      panel 0 runs on all warps; P1 of panel p+1 runs on warps 0..3
     //      (lookahead) as soon as they have updated the next pivot block,
     //      concurrently with the other trailing tiles on warps 4..7.
@@ -366,30 +376,61 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       }
       __syncthreads();
       BPH_MARK(2);
-      // ---- P3a: S[i, j] -= S[i, p] S[p, j]   (i, j outside p)
+      // ---- P3a: M[i, j] -= M[i, p] M[p, j] on the upper tiles (i, j outside p)
       {
-        const int ncw = nct - 2, total = (npan - 1) * ncw;
+        // compact numbering of the upper 32x16 tiles (ct >= 2 rt) outside
+        // panel p, row tile by row tile
+        auto upper = [&](int tI, int& rt, int& ct) {
+          for (rt = 0; rt < npan; ++rt) {
+            if (rt == p) continue;
+            const int cnt = nct - 2 * rt - (p > rt ? 2 : 0);
+            if (tI < cnt) {
+              ct = 2 * rt + tI;
+              if (p > rt && ct >= 2 * p) ct += 2;
+              return true;
+            }
+            tI -= cnt;
+          }
+          return false;
+        };
+        const int total = p * (nct - 2) - p * (p - 1) +
+                          (npan - 1 - p) * nct - (npan - 1 - p) * (npan + p);
         const bool la = p + 1 < npan;
+        const int g = lane >> 2, t4 = lane & 3;
         auto tile = [&](int tI) {
-          int rt = tI / ncw, ct = tI - rt * ncw;
-          rt += rt >= p ? 1 : 0;
-          ct += ct >= 2 * p ? 2 : 0;
+          int rt, ct;
+          upper(tI, rt, ct);
           double* Ci = R.row(32 * rt);
           double c[4][2][2];
           load_c(Ci + 16 * ct, lds, c, lane);
           tile_32x16(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
           store_c(Ci + 16 * ct, lds, c, lane);
+          if (ct >= 2 * rt + 2) {   // strictly upper: mirror into the lower triangle
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                  R.row(16 * ct + 8 * ni + 2 * t4 + k)[32 * rt + 8 * mi + g] = c[mi][ni][k];
+          }
         };
         if (!la) {
           for (int tI = warp; tI < total; tI += NW) tile(tI);
         } else {
-          // the two tiles of the next pivot block: row tile p+1 is tile row p
-          // of the compressed numbering, its column tiles 2p+2, 2p+3 -> 2p, 2p+1
-          const int la0 = p * ncw + 2 * p;
+          // the two tiles of the next pivot block (row tile p+1, column tiles
+          // 2p+2, 2p+3) come first in row p+1 of the compact numbering
+          const int la0 = p * (nct - 2) - p * (p - 1);
           if (warp < LAW) {
+#ifdef OCP_PHASE_TIMING
+            const long long tla = clock64();
+#endif
             for (int t2 = warp; t2 < 2; t2 += LAW) tile(la0 + t2);   // the two lookahead tiles
             asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
             pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, bad);
+#ifdef OCP_PHASE_TIMING
+            if (tid == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tla));
+#endif
           } else {
             for (int tI = warp - LAW; tI < total; tI += NW - LAW)
               if (tI != la0 && tI != la0 + 1) tile(tI);
@@ -398,12 +439,26 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       }
       __syncthreads();
       BPH_MARK(3);
-      // ---- P3b: column block S[i, p] = -S[i, p] Pinv, 16-row strips (each
-      //      warp reads and overwrites only its own rows)
-      for (int st = warp; st < 2 * (npan - 1); st += NW) {
-        int rt = st >> 1;
+      // ---- P3b: column block M[i, p] = M[p, i]^T (the new row block is
+      //      A^{-1} M[p][i]; by symmetry the new column block is its
+      //      transpose), pivot block -A^{-1}
+      // register transpose: task (row tile rt outside p, column half ch): lane
+      // l gathers M[p0 + 16ch + c][32rt + l], c < 16 (coalesced row reads)
+      // and writes them as 16 contiguous entries of row 32rt + l
+      for (int task = warp; task < 2 * (npan - 1); task += NW) {
+        int rt = task >> 1;
         rt += rt >= p ? 1 : 0;
-        strip_16x32(R.row(32 * rt + 16 * (st & 1)) + p0, Pinv, lds, lane);
+        const int c0 = 16 * (task & 1), i = 32 * rt + lane;
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = Prow[(c0 + c) * lds + i];
+        double* dst = R.row(i) + p0 + c0;
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(v[c], v[c + 1]);
+      }
+      for (int e = tid; e < 32 * 32; e += BF_THREADS) {   // pivot block -> -A^{-1}
+        double* q = Prow + (e >> 5) * lds + p0 + (e & 31);
+        *q = -*q;
       }
       __syncthreads();
       BPH_MARK(4);
@@ -601,7 +656,7 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
       if (lane == 0) mbar_arrive(&empty[st]);
       if (++st == BS_STAGES) { st = 0; ph ^= 1; }
     }
-    double y = (p0 + p1) + (p2 + p3);
+    double y = -((p0 + p1) + (p2 + p3));        // the store holds -W
     y += __shfl_xor_sync(0xffffffffu, y, 16);   // (S_a^{-1} vin)[i]
     if (h == 0) {
       if (fwd) {

@@ -89,6 +89,6 @@ cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes);
 // one full MGS Arnoldi step (ocp_krylov.cu); cudaErrorNotSupported if n too large
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
                            long long ldq, int j, const double* w_in, double* partials,
-                           double* h_out);
+                           double* h_out, unsigned long long* bar, unsigned long long* epoch);
 
 }  // namespace ocp

@@ -5,15 +5,17 @@
 //     for i in 0..j:  h_i = q_i . w ;  w -= h_i q_i        (modified Gram-Schmidt)
 //     h_{j+1} = ||w|| ;  q_{j+1} = w / h_{j+1}
 //
-// The MGS dependency chain (each h_i needs the w updated by h_{i-1}) is kept
-// exactly.  The grid is co-resident (cooperative launch); every thread owns a
-// fixed strided set of CH elements of w and keeps them in registers across
-// all j+1 passes, so each pass streams only q_i from HBM once: q_i is staged
-// in shared memory (CH x 512 doubles per block), the dot is reduced (block tree, then a grid barrier, then
-// every block sums the per-block partials in the same fixed order - a
-// deterministic result identical in all blocks), and the axpy reuses the
-// registers.  q_{j+1} is written unconditionally; the host ignores it on a
-// happy breakdown (krylov.py:120-122).
+// The MGS update order is kept: w is updated element by element with each
+// h_i in turn.  The grid is co-resident (cooperative launch); every thread
+// owns a fixed set of CH elements of w and keeps them in registers across all
+// j+1 passes, so each pass streams only q_i from HBM once.  Dots are reduced
+// block tree first, then every block sums the per-block partials in the same
+// fixed order (a deterministic value, identical in all blocks).  k_arnoldi_lag
+// (the config-4 path) computes the local partials of pass i+1 while the grid
+// reduction of pass i is in flight; k_arnoldi is the strided fallback for
+// vectors whose per-SM share does not fit shared memory twice.  q_{j+1} is
+// written unconditionally; the host ignores it on a happy breakdown
+// (krylov.py:120-122).
 #include <cooperative_groups.h>
 
 #include "ocp_kernels.cuh"
@@ -38,6 +40,10 @@ __device__ __forceinline__ double block_sum_all(double v, double* red) {
 }
 
 constexpr int ARN_THREADS = 512;
+#ifndef OCP_ARN_PF
+#define OCP_ARN_PF 1
+#endif
+constexpr int ARN_PF = OCP_ARN_PF;   // basis vectors prefetched into L2 ahead of the staged one
 
 // optional per-phase cycle counters of block 0 (build with -DOCP_PHASE_TIMING; tools/aphase_dbg.py)
 #ifdef OCP_PHASE_TIMING
@@ -111,26 +117,75 @@ k_arnoldi(long long n, const double* __restrict__ Q, long long ldq, int j,
   }
 }
 
-// Double-buffered variant for vectors whose per-SM share fits twice in shared
-// memory (config 4: 2 x 110 KB): block b owns the contiguous range
-// [b*per, b*per + per) and thread t its elements t + 512 k.  q_{i+1} streams
-// into the idle buffer by one TMA bulk copy issued at the start of pass i, so
-// the HBM transfer of the next basis vector runs under this pass's barrier and
-// reductions instead of after them (measured: a pass that loads q after the
-// grid barrier costs ~3x the bare HBM stream time).
+// Split grid barrier on a monotonically increasing 64-bit arrival counter
+// (target = epoch + arrivals so far; the host advances epoch by every
+// launch's arrivals; blocks are co-resident by the cooperative launch).
+// arrive releases the block's partial, wait acquires all of them.
+__device__ __forceinline__ void gbar_arrive(unsigned long long* bar) {
+  __threadfence();
+  atomicAdd(bar, 1ull);
+}
+__device__ __forceinline__ void gbar_wait(const unsigned long long* bar, unsigned long long target) {
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+  } while (v < target);
+}
+
+// two values summed over the block (fixed order), valid in every thread
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    red[wid] = a;
+    red[16 + wid] = b;
+  }
+  __syncthreads();
+  double ra = lane < ARN_THREADS / 32 ? red[lane] : 0.0;
+  double rb = lane < ARN_THREADS / 32 ? red[16 + lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ra += __shfl_xor_sync(0xffffffffu, ra, o);
+    rb += __shfl_xor_sync(0xffffffffu, rb, o);
+  }
+  return make_double2(ra, rb);
+}
+
+// MGS with the dot of pass i+1 computed while the grid reduction of pass i is
+// in flight.  With w' = w - h_i q_i (the MGS update, applied per element
+// exactly as before),
+//     q_{i+1} . w' = q_{i+1} . w - h_i (q_{i+1} . q_i),
+// so a block forms its partials A = q_{i+1} . w and B = q_{i+1} . q_i before
+// h_i is known and publishes A - h_i B the moment h_i arrives: the only
+// work left on the per-pass critical path is one FMA, the barrier and the
+// fixed-order sum of the block partials (identical in every block).  Block b
+// owns [b*per, b*per + per); q_{i+1} is staged in shared memory by one TMA
+// bulk copy issued two passes ahead and read directly from there, q_i stays in
+// registers for the axpy, and basis vectors further ahead stream into L2.
 template <int CH>
 __global__ void __launch_bounds__(ARN_THREADS, 1)
-k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
-             const double* __restrict__ w_in, double* partials, double* h_out, int per) {
-  cg::grid_group grid = cg::this_grid();
+k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
+              const double* __restrict__ w_in, double* partials, double* h_out, int per,
+              unsigned long long* bar, unsigned long long epoch) {
   extern __shared__ __align__(16) double qb[];  // [2][per]
   __shared__ double red[32];
   __shared__ __align__(8) uint64_t bars[2];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nb = gridDim.x;
   const long long b0 = (long long)blockIdx.x * per;
   const int cnt = (int)(n - b0 < per ? (n - b0 > 0 ? n - b0 : 0) : per);
   const uint32_t bytes = (uint32_t)cnt * 8u;
-  double w[CH];
+  auto load = [&](int v, int buf) {   // q_v -> shared buffer buf (thread 0)
+    if (cnt > 0) {
+      mbar_expect_tx(&bars[buf], bytes);
+      bulk_g2s(qb + buf * per, Q + (long long)v * ldq + b0, bytes, &bars[buf]);
+    }
+  };
+  double w[CH], qv[CH];
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
     const int e = tid + k * ARN_THREADS;
@@ -142,71 +197,113 @@ k_arnoldi_db(long long n, const double* __restrict__ Q, long long ldq, int j,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0 && cnt > 0) {
-    mbar_expect_tx(&bars[0], bytes);
-    bulk_g2s(qb, Q + b0, bytes, &bars[0]);
+  if (tid == 0) {
+    load(0, 0);
+    if (j >= 1) load(1, 1);
+    for (int v = 2; v <= 1 + ARN_PF && v <= j; ++v)
+      if (cnt > 0) bulk_prefetch_l2(Q + (long long)v * ldq + b0, bytes);
   }
-  const int nb = gridDim.x;
-  APH_START();
-  for (int i = 0; i <= j + 1; ++i) {
-    const bool norm_pass = (i == j + 1);
-    const double* cur = qb + (i & 1) * per;
-    double acc = 0.0;
-    // q_{i+1} goes into the buffer of q_{i-1} as soon as every thread is done
-    // with pass i-1's axpy: the HBM stream then runs under this whole pass
-    __syncthreads();
-    if (tid == 0 && i + 1 <= j && cnt > 0) {
-      uint64_t* bar = &bars[(i + 1) & 1];
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(qb + ((i + 1) & 1) * per, Q + (long long)(i + 1) * ldq + b0, bytes, bar);
+  // pass 0 head: A = q_0 . w
+  if (cnt > 0) mbar_wait(&bars[0], 0);
+  double a = 0.0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int e = tid + k * ARN_THREADS;
+    qv[k] = e < cnt ? qb[e] : 0.0;
+    a = fma(qv[k], w[k], a);
+  }
+  {
+    const double2 r = block_sum2(a, 0.0, red);
+    if (tid == 0) {
+      partials[blockIdx.x] = r.x;
+      gbar_arrive(bar);
     }
-    double qv[CH];   // q_i stays in registers for the axpy (one shared-memory read)
-    if (!norm_pass) {
-      if (cnt > 0) mbar_wait(&bars[i & 1], (i >> 1) & 1);
+  }
+  unsigned long long target = epoch;
+  APH_START();
+  for (int i = 0; i <= j; ++i) {
+    target += nb;
+    const bool more = i + 1 <= j;
+    // (1) buffer i&1 is free (q_i is in registers): stage q_{i+2}
+    __syncthreads();
+    if (tid == 0 && i + 2 <= j) {
+      load(i + 2, i & 1);
+      if (ARN_PF > 0 && i + 2 + ARN_PF <= j && cnt > 0)
+        bulk_prefetch_l2(Q + (long long)(i + 2 + ARN_PF) * ldq + b0, bytes);
+    }
+    // (2) partials of pass i+1 while barrier i is in flight
+    double2 AB = make_double2(0.0, 0.0);
+    const double* q1 = qb + ((i + 1) & 1) * per;
+    if (more) {
+      if (cnt > 0) mbar_wait(&bars[(i + 1) & 1], ((i + 1) >> 1) & 1);
       APH(0);
+      double sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int e = tid + k * ARN_THREADS;
-        qv[k] = e < cnt ? cur[e] : 0.0;
-        acc = fma(qv[k], w[k], acc);
+        const double x = e < cnt ? q1[e] : 0.0;
+        sa = fma(x, w[k], sa);
+        sb = fma(x, qv[k], sb);
       }
-    } else {
-#pragma unroll
-      for (int k = 0; k < CH; ++k) acc = fma(w[k], w[k], acc);
+      AB = block_sum2(sa, sb, red);
     }
-    const double bsum = block_sum_all<ARN_THREADS>(acc, red);
-    double* part = partials + (i & 1) * nb;
-    if (tid == 0) part[blockIdx.x] = bsum;
     APH(1);
-    grid.sync();
+    // (3) h_i: fixed-order sum of the block partials of pass i
+    if (tid == 0) gbar_wait(bar, target);
+    __syncthreads();
     APH(2);
+    const double* part = partials + (i & 1) * nb;
     double v = 0.0;
     for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
     const double h = block_sum_all<ARN_THREADS>(v, red);
     APH(3);
-    if (norm_pass) {
-      const double hn = sqrt(h);
-      if (blockIdx.x == 0 && tid == 0) h_out[i] = hn;
-      double* qn = const_cast<double*>(Q) + (long long)(j + 1) * ldq + b0;
+    // (4) publish pass i+1 (critical path: one FMA)
+    if (more && tid == 0) {
+      partials[((i + 1) & 1) * nb + blockIdx.x] = fma(-h, AB.y, AB.x);
+      gbar_arrive(bar);
+    }
+    // (5) the MGS update with h_i, then q_{i+1} into registers
+    if (blockIdx.x == 0 && tid == 0) h_out[i] = h;
+#pragma unroll
+    for (int k = 0; k < CH; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, qv[k]));
+    if (more) {
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
         const int e = tid + k * ARN_THREADS;
-        if (e < cnt) qn[e] = __ddiv_rn(w[k], hn);
+        qv[k] = e < cnt ? q1[e] : 0.0;
       }
-    } else {
-      if (blockIdx.x == 0 && tid == 0) h_out[i] = h;
-#pragma unroll
-      for (int k = 0; k < CH; ++k) w[k] = __dsub_rn(w[k], __dmul_rn(h, qv[k]));
     }
     APH(4);
+  }
+  // norm pass: h_{j+1} = ||w||, q_{j+1} = w / h_{j+1}
+  double acc = 0.0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) acc = fma(w[k], w[k], acc);
+  const double bsum = block_sum_all<ARN_THREADS>(acc, red);
+  if (tid == 0) {
+    partials[((j + 1) & 1) * nb + blockIdx.x] = bsum;
+    gbar_arrive(bar);
+    gbar_wait(bar, target + nb);
+  }
+  __syncthreads();
+  const double* part = partials + ((j + 1) & 1) * nb;
+  double v = 0.0;
+  for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
+  const double hn = sqrt(block_sum_all<ARN_THREADS>(v, red));
+  if (blockIdx.x == 0 && tid == 0) h_out[j + 1] = hn;
+  double* qn = const_cast<double*>(Q) + (long long)(j + 1) * ldq + b0;
+#pragma unroll
+  for (int k = 0; k < CH; ++k) {
+    const int e = tid + k * ARN_THREADS;
+    if (e < cnt) qn[e] = __ddiv_rn(w[k], hn);
   }
 }
 
 template <int CH>
-static cudaError_t launch_db(cudaStream_t st, int grid, int per, long long n, const double* Q,
-                             long long ldq, int j, const double* w_in, double* partials,
-                             double* h_out) {
-  void* fn = (void*)k_arnoldi_db<CH>;
+static cudaError_t launch_lag(cudaStream_t st, int grid, int per, long long n, const double* Q,
+                              long long ldq, int j, const double* w_in, double* partials,
+                              double* h_out, unsigned long long* bar, unsigned long long* epoch) {
+  void* fn = (void*)k_arnoldi_lag<CH>;
   const int smem = 2 * per * (int)sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
@@ -214,17 +311,20 @@ static cudaError_t launch_db(cudaStream_t st, int grid, int per, long long n, co
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ARN_THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorNotSupported;
+  unsigned long long ep = *epoch;
   void* args[] = {(void*)&n, (void*)&Q, (void*)&ldq, (void*)&j, (void*)&w_in, (void*)&partials,
-                  (void*)&h_out, (void*)&per};
-  return cudaLaunchCooperativeKernel(fn, grid, ARN_THREADS, args, smem, st);
+                  (void*)&h_out, (void*)&per, (void*)&bar, (void*)&ep};
+  e = cudaLaunchCooperativeKernel(fn, grid, ARN_THREADS, args, smem, st);
+  if (e == cudaSuccess) *epoch += (unsigned long long)grid * (j + 2);
+  return e;
 }
 
 // grid of co-resident blocks; returns cudaErrorNotSupported when n does not
 // fit the register-resident variant (caller falls back to per-pass kernels)
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
                            long long ldq, int j, const double* w_in, double* partials,
-                           double* h_out) {
-  // double-buffered variant when the aligned per-SM share fits twice in shared memory
+                           double* h_out, unsigned long long* bar, unsigned long long* epoch) {
+  // lagged-dot variant when the aligned per-SM share fits twice in shared memory
   {
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
@@ -236,11 +336,11 @@ cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const doub
     if (aligned && n > 0 && num_sms <= 256 && 16 * per + 512 <= optin && per <= 32 * ARN_THREADS) {
       const int p = (int)per;
       cudaError_t e;
-      if (per <= 8 * ARN_THREADS) e = launch_db<8>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
-      else if (per <= 16 * ARN_THREADS) e = launch_db<16>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
-      else if (per <= 24 * ARN_THREADS) e = launch_db<24>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
-      else if (per <= 28 * ARN_THREADS) e = launch_db<28>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
-      else e = launch_db<32>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out);
+      if (per <= 8 * ARN_THREADS) e = launch_lag<8>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else if (per <= 16 * ARN_THREADS) e = launch_lag<16>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else if (per <= 24 * ARN_THREADS) e = launch_lag<24>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else if (per <= 28 * ARN_THREADS) e = launch_lag<28>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else e = launch_lag<32>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
       if (e != cudaErrorNotSupported) return e;
       cudaGetLastError();
     }
