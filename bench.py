@@ -295,6 +295,18 @@ def run_ours(args):
                            "share_of_step": st["solve_ms"] / ms_total,
                            "algorithmic_bytes_per_launch": sol_bytes},
     }
+    # MGS Arnoldi (k_arnoldi_lag): step j reads q_0..q_j and w, writes q_{j+1}:
+    # (j + 3) vectors of 2N doubles; counted over the useful steps of every
+    # GMRES solve of the timed region (the discarded speculative step is not)
+    mgs_bytes = sum(8.0 * 2 * cfg.n * cfg.n * sum(j + 3 for j in range(m))
+                    for r in reps for m in r.gmres_iters)
+    mgs_gbs = mgs_bytes / (st["mgs_ms"] * 1e-3) / 1e9 if st["mgs_ms"] > 0 else None
+    kernels["arnoldi_mgs"] = {"bound": "hbm", "achieved": mgs_gbs, "peak": hbm, "unit": "GB/s",
+                              "frac": (mgs_gbs / hbm) if mgs_gbs and hbm else None,
+                              "launches": sum(sum(r.gmres_iters) for r in reps),
+                              "avg_ms": st["mgs_ms"] / max(sum(sum(r.gmres_iters) for r in reps), 1),
+                              "share_of_step": st["mgs_ms"] / ms_total,
+                              "algorithmic_bytes_per_solve": mgs_bytes / max(len(reps), 1)}
     dominant = max(kernels, key=lambda k: kernels[k]["share_of_step"] or 0.0)
     kd = kernels[dominant]
     traffic = load_traffic().get(dominant)
