@@ -115,10 +115,7 @@ __device__ __forceinline__ double rcp64(double x) {
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
 constexpr int WLD = 33;
-#ifndef OCP_LAW
-#define OCP_LAW 2
-#endif
-constexpr int LAW = OCP_LAW;   // lookahead warps: the next pivot inverse while the others update
+constexpr int LAW = 2;   // lookahead warps (0 and 1): the next pivot inverse while the others update
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
@@ -303,13 +300,15 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       jn0 = tid < nq ? nx[tid] : 0.0;
       jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
     }
-    if (a > 0) store_block(a - 1);
-    else __syncthreads();
     BPH_MARK(6);
     // ---- E1. M = -off^2 P W_{a-1} P = off^2 (-W_{a-1})[i^1][j^1] on the real
     //      block (the shared block holds -W_{a-1}), identity on the padding
     //      (warp per row pair, double2 columns; a pair's loads are issued
-    //      before its stores: new row i is old row i^1 with swapped columns)
+    //      before its stores: new row i is old row i^1 with swapped columns).
+    //      The loaded rows also go to the factor store: by symmetry stored
+    //      column i of line a-1 is the head of row i (coalesced streaming
+    //      stores; the shared block is read only once).
+    double* dstl = fac + (long long)(a - 1) * lsz;
     for (int i0 = 2 * warp; i0 < NPB; i0 += 2 * NW) {
       double2 v[2][4];
 #pragma unroll
@@ -319,6 +318,19 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           const int j = 2 * lane + 64 * u;
           v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(R.row(i0 + r) + j)
                                        : make_double2(0.0, 0.0);
+        }
+      if (a > 0)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = i0 + r, m16 = 16 * (i >> 4) + 16;
+          if (i >= NPS) continue;
+          double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, NPS / 16) +
+                                                    (long long)(i & 15) * (m16 + 2));
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 2 * lane + 64 * u;
+            if (j < m16) __stcs(col + (j >> 1), v[r][u]);
+          }
         }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
@@ -415,50 +427,65 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
                   R.row(16 * ct + 8 * ni + 2 * t4 + k)[32 * rt + 8 * mi + g] = c[mi][ni][k];
           }
         };
+        // ---- P3b: column block M[i, p] = M[p, i]^T (the new row block is
+        //      A^{-1} M[p][i]; by symmetry the new column block is its
+        //      transpose), pivot block -A^{-1}.  Register transpose: task
+        //      (row tile rt outside p, column half): lane l gathers
+        //      M[p0 + 16h + c][32rt + l], c < 16 (coalesced row reads) and
+        //      writes them as 16 contiguous entries of row 32rt + l.  It must
+        //      follow every P3a tile (they read the old column block).
+        auto p3b = [&](int rank, int nw) {   // rank: this warp's index among the nw doing it
+          for (int task = rank; task < 2 * (npan - 1); task += nw) {
+            int rt = task >> 1;
+            rt += rt >= p ? 1 : 0;
+            const int c0 = 16 * (task & 1), i = 32 * rt + lane;
+            double v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = Prow[(c0 + c) * lds + i];
+            double* dst = R.row(i) + p0 + c0;
+#pragma unroll
+            for (int c = 0; c < 16; c += 2)
+              *reinterpret_cast<double2*>(dst + c) = make_double2(v[c], v[c + 1]);
+          }
+          for (int e = 32 * rank + lane; e < 32 * 32; e += 32 * nw) {   // pivot block -> -A^{-1}
+            double* q = Prow + (e >> 5) * lds + p0 + (e & 31);
+            *q = -*q;
+          }
+        };
         if (!la) {
           for (int tI = warp; tI < total; tI += NW) tile(tI);
+          __syncthreads();
+          BPH_MARK(3);
+          p3b(warp, NW);
         } else {
           // the two tiles of the next pivot block (row tile p+1, column tiles
-          // 2p+2, 2p+3) come first in row p+1 of the compact numbering
+          // 2p+2, 2p+3) come first in row p+1 of the compact numbering; the
+          // lookahead warps then invert that block while the others finish
+          // the trailing tiles and do P3b (barrier 5: all P3a tiles done)
           const int la0 = p * (nct - 2) - p * (p - 1);
-          if (warp < LAW) {
+          // (lookahead warps 0 and 4, one SM sub-partition, measured 13 % slower)
+          const bool law = warp < LAW;
+          const int lrank = warp, trank = warp - LAW;
+          if (law) {
 #ifdef OCP_PHASE_TIMING
             const long long tla = clock64();
 #endif
-            for (int t2 = warp; t2 < 2; t2 += LAW) tile(la0 + t2);   // the two lookahead tiles
+            tile(la0 + lrank);   // the two lookahead tiles
+            asm volatile("bar.arrive 5, %0;" ::"n"(BF_THREADS) : "memory");
             asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
-            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, bad);
+            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad);
 #ifdef OCP_PHASE_TIMING
             if (tid == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tla));
 #endif
           } else {
-            for (int tI = warp - LAW; tI < total; tI += NW - LAW)
+            for (int tI = trank; tI < total; tI += NW - LAW)
               if (tI != la0 && tI != la0 + 1) tile(tI);
+            asm volatile("bar.sync 5, %0;" ::"n"(BF_THREADS) : "memory");
+            p3b(trank, NW - LAW);
           }
+          __syncthreads();
+          BPH_MARK(3);
         }
-      }
-      __syncthreads();
-      BPH_MARK(3);
-      // ---- P3b: column block M[i, p] = M[p, i]^T (the new row block is
-      //      A^{-1} M[p][i]; by symmetry the new column block is its
-      //      transpose), pivot block -A^{-1}
-      // register transpose: task (row tile rt outside p, column half ch): lane
-      // l gathers M[p0 + 16ch + c][32rt + l], c < 16 (coalesced row reads)
-      // and writes them as 16 contiguous entries of row 32rt + l
-      for (int task = warp; task < 2 * (npan - 1); task += NW) {
-        int rt = task >> 1;
-        rt += rt >= p ? 1 : 0;
-        const int c0 = 16 * (task & 1), i = 32 * rt + lane;
-        double v[16];
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = Prow[(c0 + c) * lds + i];
-        double* dst = R.row(i) + p0 + c0;
-#pragma unroll
-        for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(dst + c) = make_double2(v[c], v[c + 1]);
-      }
-      for (int e = tid; e < 32 * 32; e += BF_THREADS) {   // pivot block -> -A^{-1}
-        double* q = Prow + (e >> 5) * lds + p0 + (e & 31);
-        *q = -*q;
       }
       __syncthreads();
       BPH_MARK(4);
