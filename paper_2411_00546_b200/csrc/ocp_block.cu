@@ -546,11 +546,11 @@ int block_factor_smem_bytes(int max_npb) {
 // ---------------------------------------------------------------------------
 // One stage of the solve ring holds two tile columns of a line, c and
 // cpb-1-c (the middle one alone when cpb is odd), so every stage carries the
-// same bytes (~90 KB in flight per CTA).  Stages are sized for pairs up to
-// cpb = 10 (two CTAs per SM); a subdomain whose pairs do not fit streams one
-// tile column per stage.
+// same bytes (~90-100 KB in flight per CTA).  Stages are sized for pairs up
+// to cpb = 11 (config 4's corner: two CTAs per SM still fit); a subdomain
+// whose pairs do not fit streams one tile column per stage.
 __host__ __device__ inline int bs_stage_doubles(int max_nps) {
-  const int cpb = max_nps / 16, pc = cpb < 10 ? cpb : 10;
+  const int cpb = max_nps / 16, pc = cpb < 11 ? cpb : 11;
   const int pair = 256 * pc + 320, single = (int)block_col_doubles(cpb - 1);
   return pair > single ? pair : single;
 }
