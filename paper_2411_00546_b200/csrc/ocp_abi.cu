@@ -22,7 +22,7 @@
 
 using namespace ocp;
 namespace ocp { void read_phase(unsigned long long* out); void read_bphase(unsigned long long* out);
-                void read_aphase(unsigned long long* out); }
+                void read_aphase(unsigned long long* out); void read_subt(long long* out, int n); }
 
 namespace {
 
@@ -1443,6 +1443,10 @@ int ocp_reset_stats(ocp_ctx* ctx) {
 }
 
 #ifdef OCP_PHASE_TIMING
+int ocp_debug_subt(long long* out, int n) {
+  ocp::read_subt(out, n);
+  return 0;
+}
 int ocp_debug_phase(unsigned long long* out) {
   ocp::read_phase(out);
   ocp::read_bphase(out + 8);

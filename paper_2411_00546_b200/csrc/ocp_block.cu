@@ -55,8 +55,12 @@ __device__ unsigned long long g_bphase[8];
       t_last = now;                                                                     \
     }                                                                                   \
   } while (0)
+__device__ long long g_subt[1024][3];   // per subdomain: start clock, end clock, SM id
 void read_bphase(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, g_bphase, 8 * sizeof(unsigned long long));
+}
+void read_subt(long long* out, int n) {
+  cudaMemcpyFromSymbol(out, g_subt, (size_t)3 * (n < 1024 ? n : 1024) * sizeof(long long));
 }
 #else
 #define BPH_START() (void)0
@@ -516,6 +520,9 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     double* fac = fac_pool + s.fac;
     const int lds = s.pad_ + 4;
     if (threadIdx.x == 0) bad = 0;
+#ifdef OCP_PHASE_TIMING
+    long long t_sub = clock64();
+#endif
     __syncthreads();
     // shared memory: [S rows: SMEM_S doubles][W0, W1: 32 x 33][JL]
     constexpr int SMEM_S = BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4);
@@ -531,6 +538,17 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
                        &bad, W0, W1, JL);
     }
     __syncthreads();
+#ifdef OCP_PHASE_TIMING
+    if (threadIdx.x == 0 && sid < 1024) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      long long g0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      g_subt[sid][0] = t_sub;
+      g_subt[sid][1] = clock64();
+      g_subt[sid][2] = smid;
+    }
+#endif
     if (threadIdx.x == 0) status[sid] = bad;
     __syncthreads();
   }
