@@ -832,6 +832,15 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
   Timer tj(ctx, CLS_JVP);
+  if (ctx->fmt == 1) {   // one fused launch: rhs from d, solve, out[own] = -(d + x)
+    double bytes = 0;
+    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
+    Timer t(ctx, CLS_SOLVE, 0, bytes);
+    CK(launch_block_solve(2, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
+                          ctx->P.off, ctx->maxNPS, d, out, ctx->P.n));
+    ++ctx->launches;
+    return OCP_OK;
+  }
   const dim3 grid(I, 4);
   k_jvp_rhs<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B);
   CKL();

@@ -585,10 +585,36 @@ __host__ __device__ inline int bs_threads(int max_nps) { return 2 * max_nps + 32
 // through the ring independently: a producer warp refills a slot once every
 // consumer warp has released it (empty mbarriers), and the consumers meet
 // once per line (named barrier 1) because line a+1 needs all of line a.
+// JVP right-hand side of local point t (= 2b + f) of oriented line a: the
+// coupling to the outside of the rectangle, e = A_ext d (schwarz.py:341-342),
+// in k_jvp_rhs's operation order (zero for points with no outside neighbour)
+__device__ __forceinline__ double jvp_rhs(const SubInfo& s, const double* d, int gn, double off,
+                                          int a, int t) {
+  const int b = t >> 1, f = t & 1;
+  int i, j;
+  local_to_global(s, a, b, i, j);
+  const long long Ntot = (long long)gn * gn;
+  const int di[4] = {-1, 0, 0, 1};
+  const int dj[4] = {0, -1, 1, 0};
+  double e = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int ii = i + di[u], jj = j + dj[u];
+    if (ii < 0 || ii >= gn || jj < 0 || jj >= gn || in_rect(s, ii, jj)) continue;
+    e = add(e, mul(off, d[f * Ntot + (long long)ii * gn + jj]));
+  }
+  return e;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(BS_MAX_THREADS, 2)
 k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
-              double scale, double* out_pool, double off, int max_npb) {
+              double scale, double* out_pool, double off, int max_npb, const double* dglob,
+              double* oglob, int gn) {
+  // MODE 0: solve pool -> pool.  MODE 1: the backward sweep stops at the first
+  // owned line (JVP / RAS apply).  MODE 2: the fused JVP (schwarz.py:327-345):
+  // MODE 1 with the right-hand side A_ext d computed from the global d and
+  // out[own] = -(d + x)[own] written straight to the global vector.
   extern __shared__ __align__(16) double sm[];
   const SubInfo s = subs[list[blockIdx.x]];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -605,7 +631,7 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
   const bool paired = 256 * cpb + 320 <= SBS;
   const int nst = paired ? (cpb + 1) / 2 : cpb;       // stages per line
   int a_stop = 0;
-  if (MODE == 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+  if (MODE >= 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
   const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;   // lines a = nr-2 .. a_stop
   const int nlines = nr + nback, total = nlines * nst;
   if (tid == 0) {
@@ -616,7 +642,8 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // line 0 input, stored permuted: vp[t ^ 1] = vin[t]
-  for (int t = tid; t < NPS; t += blockDim.x) vp[t ^ 1] = t < n ? scale * in[t] : 0.0;
+  for (int t = tid; t < NPS; t += blockDim.x)
+    vp[t ^ 1] = t < n ? (MODE == 2 ? jvp_rhs(s, dglob, gn, off, 0, t) : scale * in[t]) : 0.0;
   __syncthreads();
   if (warp == (int)(blockDim.x >> 5) - 1) {
     // ---- producer: stage t = (line blk, k) into slot t % BS_STAGES
@@ -661,7 +688,7 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
     double nxt = 0.0;
     if (h == 0 && i < n) {
       if (fwd) {
-        if (a + 1 < nr) nxt = in[(long long)(a + 1) * n + i];
+        if (a + 1 < nr) nxt = MODE == 2 ? jvp_rhs(s, dglob, gn, off, a + 1, i) : in[(long long)(a + 1) * n + i];
       } else {
         nxt = out[(long long)a * n + i];
       }
@@ -704,17 +731,28 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
     double y = -((p0 + p1) + (p2 + p3));        // the store holds -W
     y += __shfl_xor_sync(0xffffffffu, y, 16);   // (S_a^{-1} vin)[i]
     if (h == 0) {
+      double x = 0.0;   // x_a where this line is final (backward, or the last line)
       if (fwd) {
         // w_a = y; next input = scale in_{a+1} - off w_a (the last line starts
         // the backward sweep with x_{nr-1} = w_{nr-1})
         const double w = i < n ? y : 0.0;
-        if (i < n) out[(long long)a * n + i] = w;
+        if (i < n && (MODE != 2 || a + 1 < nr)) out[(long long)a * n + i] = w;
         vnext[i ^ 1] = (a + 1 < nr) ? (i < n ? fma(-off, w, scale * nxt) : 0.0) : w;
+        x = w;
       } else {
         // x_a = w_a - off y ; next input = x_a
-        const double x = i < n ? fma(-off, y, nxt) : 0.0;
-        if (i < n) out[(long long)a * n + i] = x;
+        x = i < n ? fma(-off, y, nxt) : 0.0;
+        if (MODE != 2 && i < n) out[(long long)a * n + i] = x;
         vnext[i ^ 1] = x;
+      }
+      if (MODE == 2 && (!fwd || a + 1 == nr) && i < n) {
+        // out[own] = -(d_loc + x)[own]  (k_jvp_out's rounding)
+        int gi, gj;
+        local_to_global(s, a, i >> 1, gi, gj);
+        if (gi >= s.or0 && gi < s.or1 && gj >= s.oc0 && gj < s.oc1) {
+          const long long g = (long long)(i & 1) * gn * gn + (long long)gi * gn + gj;
+          oglob[g] = -add(dglob[g], x);
+        }
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * cpb) : "memory");
@@ -727,14 +765,20 @@ size_t block_solve_smem_bytes(int max_npb) {
 
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
                                const int* list, const double* fac, const double* in, double scale,
-                               double* out_pool, double off, int max_npb) {
+                               double* out_pool, double off, int max_npb, const double* dglob,
+                               double* oglob, int gn) {
   const size_t smem = block_solve_smem_bytes(max_npb);
   const int nt = bs_threads(max_npb);
   if (nt > BS_MAX_THREADS) return cudaErrorInvalidConfiguration;
   if (mode == 0)
-    k_block_solve<0><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+    k_block_solve<0><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
+                                             dglob, oglob, gn);
+  else if (mode == 1)
+    k_block_solve<1><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
+                                             dglob, oglob, gn);
   else
-    k_block_solve<1><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb);
+    k_block_solve<2><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
+                                             dglob, oglob, gn);
   return cudaGetLastError();
 }
 
@@ -744,7 +788,9 @@ cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes) {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_block_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_block_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  e = cudaFuncSetAttribute(k_block_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_block_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
 }
 
 }  // namespace ocp

@@ -84,7 +84,8 @@ int block_factor_smem_bytes(int max_npb);
 size_t block_solve_smem_bytes(int max_npb);
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
                                const int* list, const double* fac, const double* in, double scale,
-                               double* out_pool, double off, int max_npb);
+                               double* out_pool, double off, int max_npb,
+                               const double* dglob = nullptr, double* oglob = nullptr, int gn = 0);
 cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes);
 // one full MGS Arnoldi step (ocp_krylov.cu); cudaErrorNotSupported if n too large
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
