@@ -171,7 +171,7 @@ class _RetiredCache:
     """Buffers of destroyed engines (their streams are idle), reused by size
     across engines like a caching allocator; bounded, thread-safe."""
 
-    def __init__(self, limit_bytes=24 << 30):
+    def __init__(self, limit_bytes=16 << 30):
         self.free = {}
         self.cached = 0
         self.limit = limit_bytes

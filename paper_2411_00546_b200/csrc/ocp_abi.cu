@@ -441,7 +441,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     // the pool keeps the pages for the next context instead of unmapping them
     cudaMemPool_t mp;
     if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
-      unsigned long long thr = 48ULL << 30;
+      unsigned long long thr = 16ULL << 30;
       cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
