@@ -18,6 +18,14 @@ cfg, spec, dec, sched = bench.problem()
 newton_cfg = NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1)
 kry = KrylovConfig(rel_tol=1e-8, max_iters=1000)
 x0 = np.zeros(cfg.unknowns)
+if "--bench-state" in sys.argv[1:] or True:
+    # like bench.py: a device-resident engine stays alive through the e2e steps
+    from paper_2411_00546_b200.schwarz import solve_on_device
+    main = build_local_systems(dec, spec)
+    xd = main.from_host(x0)
+    for _ in range(2):
+        solve_on_device(main, xd, sched, newton_cfg, kry, 1e-7, 200)
+    main.sync()
 for rep in range(5):
     fresh = ProblemSpec(grid=spec.grid, a=None, phi=spec.phi, nu=spec.nu, mu=spec.mu,
                         f=spec.f.copy(), y_d=spec.y_d.copy())
@@ -34,5 +42,10 @@ for rep in range(5):
           f"(sweep {st['sweep_ms']:.1f} jvp {st['jvp_ms']:.1f} mgs {st['mgs_ms']:.1f}, sum {dev:.1f}), "
           f"conv {r.converged}", flush=True)
     dec.__dict__.get("_engines", {}).pop(id(fresh), None)
+    import weakref
+    wr = weakref.ref(eng)
     del fresh, eng, x
     gc.collect()
+    if wr() is not None:
+        refs = gc.get_referrers(wr())
+        print("  engine still alive; referrers:", [type(o).__name__ + (str(list(o.keys())[:6]) if isinstance(o, dict) else "") for o in refs][:8], flush=True)
