@@ -255,7 +255,7 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, (cnt + 1) * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
     const int grid = std::min(cnt, ctx->bf_grid);
-    k_block_factor<<<grid, 256, block_factor_smem_bytes(ctx->maxNPB), ctx->stream>>>(
+    k_block_factor<<<grid, block_factor_threads(), block_factor_smem_bytes(ctx->maxNPB), ctx->stream>>>(
         ctx->d_subs, ctx->d_flist, cnt, ctx->P, ctx->JD, fac, ctx->bscratch, ctx->bs_stride,
         ctx->d_status);
     CKL();

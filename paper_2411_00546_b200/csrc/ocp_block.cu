@@ -42,7 +42,10 @@
 
 namespace ocp {
 
-constexpr int BF_THREADS = 256;
+#ifndef OCP_BF_THREADS
+#define OCP_BF_THREADS 384
+#endif
+constexpr int BF_THREADS = OCP_BF_THREADS;   // factor CTA: 12 warps (measured: 8 warps 5 % slower, 16 warps 1 % slower)
 
 #ifdef OCP_PHASE_TIMING
 __device__ unsigned long long g_bphase[8];
@@ -119,7 +122,10 @@ __device__ __forceinline__ double rcp64(double x) {
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
 constexpr int WLD = 33;
-constexpr int LAW = 2;   // lookahead warps (0 and 1): the next pivot inverse while the others update
+#ifndef OCP_LAW
+#define OCP_LAW 4
+#endif
+constexpr int LAW = OCP_LAW;   // lookahead warps (0 .. LAW-1): the next pivot inverse while the others update
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
                                              int lane, int* bad) {
@@ -376,7 +382,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     //      panel 0 runs on all warps; P1 of panel p+1 runs on warps 0..3
     //      (lookahead) as soon as they have updated the next pivot block,
     //      concurrently with the other trailing tiles on warps 4..7.
-    pivot_inverse32<8>(R.row(0), lds, W0, W1, warp, lane, bad);
+    if (warp < 8) pivot_inverse32<8>(R.row(0), lds, W0, W1, warp, lane, bad);
     __syncthreads();
     BPH_MARK(5);
     for (int p = 0; p < npan; ++p) {
@@ -474,7 +480,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
 #ifdef OCP_PHASE_TIMING
             const long long tla = clock64();
 #endif
-            tile(la0 + lrank);   // the two lookahead tiles
+            if (lrank < 2) tile(la0 + lrank);   // the two lookahead tiles
             asm volatile("bar.arrive 5, %0;" ::"n"(BF_THREADS) : "memory");
             asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
             pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad);
@@ -553,6 +559,8 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     __syncthreads();
   }
 }
+
+int block_factor_threads() { return BF_THREADS; }
 
 int block_factor_smem_bytes(int max_npb) {
   (void)max_npb;   // fixed layout: [S: 160 x 164][W0, W1: 32 x 33]
