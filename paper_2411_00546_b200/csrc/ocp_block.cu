@@ -548,8 +548,6 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     if (threadIdx.x == 0 && sid < 1024) {
       unsigned smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      long long g0;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
       g_subt[sid][0] = t_sub;
       g_subt[sid][1] = clock64();
       g_subt[sid][2] = smid;
