@@ -356,3 +356,53 @@ def test_band_and_block_factor_formats_agree(name, monkeypatch):
     assert rel_l2(xb, xk) <= 1e-10
     n2 = cfg.n * cfg.n
     assert rel_l2(xk[:n2], g["y"]) <= 1e-8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_fused_jvp_matches_unfused_band_path(name, monkeypatch):
+    """The fused block-format JVP (one launch: rhs from d, solve, out[own] =
+    -(d + x)) against the band format's separate rhs / solve / out kernels on
+    the same sweep: the same operator to round-off, on random directions."""
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep
+    cfg = CONFIGS[name]
+    spec = build_spec(cfg, with_matrix=False)
+    outs = {}
+    for fmt in ("band", "block"):
+        monkeypatch.setenv("OCP_FACTOR_FORMAT", fmt)
+        dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+        eng = build_local_systems(dec, spec)
+        x = eng.from_host(np.zeros(cfg.unknowns))
+        fac = eng.factor_store()
+        _sweep(eng, x, fac, ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min),
+               NewtonConfig(tol=1e-7, max_outer=200))
+        rng = np.random.default_rng(7)
+        outs[fmt] = [_jvp(eng, fac, eng.from_host(rng.standard_normal(cfg.unknowns))).to_host()
+                     for _ in range(2)]
+    for a, b in zip(outs["band"], outs["block"]):
+        assert rel_l2(b, a) <= 1e-11
+
+
+@pytest.mark.gpu
+def test_fresh_contexts_reuse_memory_and_agree_bitwise():
+    """Solves on successive fresh contexts (device buffers retired to the
+    process cache, the GMRES basis from the stream-ordered pool) give
+    bitwise-identical iterates and reports."""
+    import gc
+    cfg = CONFIGS["cfg2"]
+    spec = build_spec(cfg, with_matrix=False)
+    res = []
+    for _ in range(3):
+        fresh = type(spec)(grid=spec.grid, a=None, phi=spec.phi, nu=spec.nu, mu=spec.mu,
+                           f=spec.f.copy(), y_d=spec.y_d.copy())
+        dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+        x, rep = raspen_solve(np.zeros(cfg.unknowns), dec, fresh,
+                              ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min),
+                              cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+                              krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000), inner_tol=1e-8)
+        res.append((x, rep.gmres_iters, rep.inner_iters))
+        del dec, fresh
+        gc.collect()
+    for x, g_it, i_it in res[1:]:
+        np.testing.assert_array_equal(x, res[0][0])
+        assert g_it == res[0][1] and i_it == res[0][2]
