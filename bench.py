@@ -263,6 +263,8 @@ def run_ours(args):
                                   inner_tol=INNER_TOL)
             if it > 0:
                 e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            print(f"e2e step {it}: {(time.perf_counter() - t0) * 1e3:.1f} ms"
+                  + (" (warm-up)" if it == 0 else ""), file=sys.stderr, flush=True)
             assert rep.converged, rep.failure
             dec.__dict__.get("_engines", {}).pop(id(fresh), None)
             del fresh, x
