@@ -310,6 +310,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       jn0 = tid < nq ? nx[tid] : 0.0;
       jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
     }
+    __syncthreads();   // JL complete: both warp groups read all of it in E2
     BPH_MARK(6);
     // ---- E1. M = -off^2 P W_{a-1} P = off^2 (-W_{a-1})[i^1][j^1] on the real
     //      block (the shared block holds -W_{a-1}), identity on the padding
@@ -319,7 +320,13 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     //      column i of line a-1 is the head of row i (coalesced streaming
     //      stores; the shared block is read only once).
     double* dstl = fac + (long long)(a - 1) * lsz;
-    for (int i0 = 2 * warp; i0 < NPB; i0 += 2 * NW) {
+    // warps 0..LAW-1 build rows 0..31 and invert the first pivot block while
+    // the other warps build the remaining rows (3 % faster than E for all
+    // rows, then the first pivot inverse on 8 warps)
+    const bool grpA = warp < LAW;
+    const int e_lo = grpA ? 0 : 32, e_hi = grpA ? 32 : NPB;
+    const int e_w = grpA ? warp : warp - LAW, e_nw = grpA ? LAW : NW - LAW;
+    for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw) {
       double2 v[2][4];
 #pragma unroll
       for (int r = 0; r < 2; ++r)
@@ -362,12 +369,19 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
         }
       }
     }
-    __syncthreads();
+    if (grpA) asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
+    else asm volatile("bar.sync 3, %0;" ::"n"(BF_THREADS - 32 * LAW) : "memory");
     BPH_MARK(7);
-    // ---- E2. + P D_a: (P D_a)[i][j] = D_a[i^1][j], seven diagonals
-    for (int e = tid; e < 7 * n; e += BF_THREADS) {
-      const int i = e / 7, j = i + (e - 7 * i) - 3;
-      if (j >= 0 && j < n) R.row(i)[j] += d_entry(s, JL, i ^ 1, j, off);
+    {
+      const int n_hi = e_hi < n ? e_hi : n;
+      for (int e = 7 * e_lo + 32 * e_w + lane; e < 7 * n_hi; e += 32 * e_nw) {
+        const int i = e / 7, j = i + (e - 7 * i) - 3;
+        if (j >= 0 && j < n) R.row(i)[j] += d_entry(s, JL, i ^ 1, j, off);
+      }
+    }
+    if (grpA) {
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
+      pivot_inverse32<LAW>(R.row(0), lds, W0, W1, warp, lane, bad);
     }
     __syncthreads();
     BPH_MARK(1);
@@ -378,12 +392,10 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     //        P3a  M[i][j] -= M[i][p] M[p][j]           upper 32x16 tiles only (DMMA);
     //             strictly-upper tiles are mirrored into the lower triangle
     //        P3b  M[i][p] = M[p][i]^T (transposed copy), M[p][p] = -A^{-1}
-    //      P1 of
-    //      panel 0 runs on all warps; P1 of panel p+1 runs on warps 0..3
-    //      (lookahead) as soon as they have updated the next pivot block,
-    //      concurrently with the other trailing tiles on warps 4..7.
-    if (warp < 8) pivot_inverse32<8>(R.row(0), lds, W0, W1, warp, lane, bad);
-    __syncthreads();
+    //      P1 (the 32x32 pivot inverse) of panel 0 ran on warps 0..LAW-1 under
+    //      the E phase; P1 of panel p+1 runs on the same warps (lookahead) as
+    //      soon as warps 0, 1 have updated the next pivot block, concurrently
+    //      with the other trailing tiles.
     BPH_MARK(5);
     for (int p = 0; p < npan; ++p) {
       const int p0 = 32 * p;
