@@ -72,6 +72,7 @@ struct ocp_ctx {
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
   unsigned long long* arn_bar = nullptr;   // split grid barrier of the Arnoldi kernel
+  double* arn_partials = nullptr;          // [2][2048] block partials of the Arnoldi kernel
   unsigned long long arn_epoch = 0;        // arrivals so far on arn_bar
   double* gm_Q = nullptr;      // persistent GMRES basis (grow-only), ocp_raspen_gmres
   double* gm_w = nullptr;
@@ -520,6 +521,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(cudaMalloc(&ctx->red_counter, sizeof(unsigned int)));
   CKC(cudaMemset(ctx->red_counter, 0, sizeof(unsigned int)));
   CKC(cudaMalloc(&ctx->arn_bar, sizeof(unsigned long long)));
+  CKC(cudaMalloc(&ctx->arn_partials, 2 * 2048 * sizeof(double)));
   CKC(cudaMemset(ctx->arn_bar, 0, sizeof(unsigned long long)));
   CKC(cudaMalloc(&ctx->d_result, 8 * sizeof(double)));
   ctx->h_cap = 4096;
@@ -575,7 +577,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
                   (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
-                  (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->d_result,
+                  (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
                   (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist, (void*)ctx->d_solve_order,
@@ -1008,7 +1010,7 @@ int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j, cons
   cudaStream_t st = ctx->stream;
   {
     Timer t(ctx, CLS_MGS);
-    cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, ldq, j, w_in, ctx->red_partials, ctx->d_h,
+    cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, ldq, j, w_in, ctx->arn_partials, ctx->d_h,
                                    ctx->arn_bar, &ctx->arn_epoch);
     if (e == cudaSuccess) {
       ++ctx->launches;
@@ -1308,7 +1310,7 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
     double* dh = ctx->gm_dh + (jj & 1) * hs;
     if (pipelined) {
       Timer t(ctx, CLS_MGS);
-      cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, n, jj, w, ctx->red_partials, dh,
+      cudaError_t e = launch_arnoldi(st, ctx->num_sms, n, Q, n, jj, w, ctx->arn_partials, dh,
                                      ctx->arn_bar, &ctx->arn_epoch);
       if (e == cudaSuccess) {
         ++ctx->launches;

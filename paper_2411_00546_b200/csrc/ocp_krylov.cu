@@ -40,6 +40,11 @@ __device__ __forceinline__ double block_sum_all(double v, double* red) {
 }
 
 constexpr int ARN_THREADS = 512;
+#ifndef OCP_LAG_THREADS
+#define OCP_LAG_THREADS 512
+#endif
+constexpr int LAG_THREADS = OCP_LAG_THREADS;          // lagged kernel: threads per block (256 x 2 per SM measured 2 % slower)
+constexpr int LAG_BPSM = 512 / LAG_THREADS;           // and blocks per SM
 #ifndef OCP_ARN_SLEEP
 #define OCP_ARN_SLEEP 50   // ns between barrier polls (measured ~2 % faster than spinning)
 #endif
@@ -140,6 +145,7 @@ __device__ __forceinline__ void gbar_wait(const unsigned long long* bar, unsigne
 }
 
 // two values summed over the block (fixed order), valid in every thread
+template <int THREADS>
 __device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -153,8 +159,8 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
     red[16 + wid] = b;
   }
   __syncthreads();
-  double ra = lane < ARN_THREADS / 32 ? red[lane] : 0.0;
-  double rb = lane < ARN_THREADS / 32 ? red[16 + lane] : 0.0;
+  double ra = lane < THREADS / 32 ? red[lane] : 0.0;
+  double rb = lane < THREADS / 32 ? red[16 + lane] : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ra += __shfl_xor_sync(0xffffffffu, ra, o);
@@ -175,7 +181,7 @@ __device__ __forceinline__ double2 block_sum2(double a, double b, double* red) {
 // bulk copy issued two passes ahead and read directly from there, q_i stays in
 // registers for the axpy, and basis vectors further ahead stream into L2.
 template <int CH>
-__global__ void __launch_bounds__(ARN_THREADS, 1)
+__global__ void __launch_bounds__(LAG_THREADS, LAG_BPSM)
 k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
               const double* __restrict__ w_in, double* partials, double* h_out, int per,
               unsigned long long* bar, unsigned long long epoch) {
@@ -195,7 +201,7 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
   double w[CH], qv[CH];
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
-    const int e = tid + k * ARN_THREADS;
+    const int e = tid + k * LAG_THREADS;
     w[k] = e < cnt ? w_in[b0 + e] : 0.0;
   }
   if (tid == 0) {
@@ -215,12 +221,12 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
   double a = 0.0;
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
-    const int e = tid + k * ARN_THREADS;
+    const int e = tid + k * LAG_THREADS;
     qv[k] = e < cnt ? qb[e] : 0.0;
     a = fma(qv[k], w[k], a);
   }
   {
-    const double2 r = block_sum2(a, 0.0, red);
+    const double2 r = block_sum2<LAG_THREADS>(a, 0.0, red);
     if (tid == 0) {
       partials[blockIdx.x] = r.x;
       gbar_arrive(bar);
@@ -247,12 +253,12 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
       double sa = 0.0, sb = 0.0;
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
-        const int e = tid + k * ARN_THREADS;
+        const int e = tid + k * LAG_THREADS;
         const double x = e < cnt ? q1[e] : 0.0;
         sa = fma(x, w[k], sa);
         sb = fma(x, qv[k], sb);
       }
-      AB = block_sum2(sa, sb, red);
+      AB = block_sum2<LAG_THREADS>(sa, sb, red);
     }
     APH(1);
     // (3) h_i: fixed-order sum of the block partials of pass i
@@ -262,7 +268,7 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
     const double* part = partials + (i & 1) * nb;
     double v = 0.0;
     for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
-    const double h = block_sum_all<ARN_THREADS>(v, red);
+    const double h = block_sum_all<LAG_THREADS>(v, red);
     APH(3);
     // (4) publish pass i+1 (critical path: one FMA)
     if (more && tid == 0) {
@@ -276,7 +282,7 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
     if (more) {
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
-        const int e = tid + k * ARN_THREADS;
+        const int e = tid + k * LAG_THREADS;
         qv[k] = e < cnt ? q1[e] : 0.0;
       }
     }
@@ -286,7 +292,7 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
   double acc = 0.0;
 #pragma unroll
   for (int k = 0; k < CH; ++k) acc = fma(w[k], w[k], acc);
-  const double bsum = block_sum_all<ARN_THREADS>(acc, red);
+  const double bsum = block_sum_all<LAG_THREADS>(acc, red);
   if (tid == 0) {
     partials[((j + 1) & 1) * nb + blockIdx.x] = bsum;
     gbar_arrive(bar);
@@ -296,12 +302,12 @@ k_arnoldi_lag(long long n, const double* __restrict__ Q, long long ldq, int j,
   const double* part = partials + ((j + 1) & 1) * nb;
   double v = 0.0;
   for (int b = tid; b < nb; b += blockDim.x) v += __ldcg(part + b);
-  const double hn = sqrt(block_sum_all<ARN_THREADS>(v, red));
+  const double hn = sqrt(block_sum_all<LAG_THREADS>(v, red));
   if (blockIdx.x == 0 && tid == 0) h_out[j + 1] = hn;
   double* qn = const_cast<double*>(Q) + (long long)(j + 1) * ldq + b0;
 #pragma unroll
   for (int k = 0; k < CH; ++k) {
-    const int e = tid + k * ARN_THREADS;
+    const int e = tid + k * LAG_THREADS;
     if (e < cnt) qn[e] = __ddiv_rn(w[k], hn);
   }
 }
@@ -315,13 +321,13 @@ static cudaError_t launch_lag(cudaStream_t st, int grid, int per, long long n, c
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ARN_THREADS, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LAG_THREADS, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorNotSupported;
   unsigned long long ep = *epoch;
   void* args[] = {(void*)&n, (void*)&Q, (void*)&ldq, (void*)&j, (void*)&w_in, (void*)&partials,
                   (void*)&h_out, (void*)&per, (void*)&bar, (void*)&ep};
-  e = cudaLaunchCooperativeKernel(fn, grid, ARN_THREADS, args, smem, st);
+  e = cudaLaunchCooperativeKernel(fn, grid, LAG_THREADS, args, smem, st);
   if (e == cudaSuccess) *epoch += (unsigned long long)grid * (j + 2);
   return e;
 }
@@ -336,18 +342,18 @@ cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const doub
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    long long per = (n + num_sms - 1) / num_sms;
+    const int lgrid = num_sms * LAG_BPSM;
+    long long per = (n + lgrid - 1) / lgrid;
     per += per & 1;
     const bool aligned = (n % 2 == 0) && (ldq % 2 == 0) &&
                          ((reinterpret_cast<uintptr_t>(Q) & 15) == 0);
-    if (aligned && n > 0 && num_sms <= 256 && 16 * per + 512 <= optin && per <= 32 * ARN_THREADS) {
+    if (aligned && n > 0 && lgrid <= 1024 && LAG_BPSM * (16 * per + 1024) <= optin && per <= 28 * LAG_THREADS) {
       const int p = (int)per;
       cudaError_t e;
-      if (per <= 8 * ARN_THREADS) e = launch_lag<8>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
-      else if (per <= 16 * ARN_THREADS) e = launch_lag<16>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
-      else if (per <= 24 * ARN_THREADS) e = launch_lag<24>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
-      else if (per <= 28 * ARN_THREADS) e = launch_lag<28>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
-      else e = launch_lag<32>(st, num_sms, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      if (per <= 8 * LAG_THREADS) e = launch_lag<8>(st, lgrid, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else if (per <= 16 * LAG_THREADS) e = launch_lag<16>(st, lgrid, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else if (per <= 24 * LAG_THREADS) e = launch_lag<24>(st, lgrid, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
+      else e = launch_lag<28>(st, lgrid, p, n, Q, ldq, j, w_in, partials, h_out, bar, epoch);
       if (e != cudaErrorNotSupported) return e;
       cudaGetLastError();
     }
