@@ -199,7 +199,7 @@ def config_block(cfg):
         "inner_tol": INNER_TOL,
         "deviation": "inner_tol 1e-7 on both arms: the reference fails config 4 at 1e-8 "
                      "(LocalSolveError, FP64 residual floor; SURVEY.md 0.13)",
-        "l2": "inputs larger than L2 (8 GB stored local factors streamed by every JVP)",
+        "l2": "inputs larger than L2 (2.3 GB stored local factors streamed by every JVP)",
     }
 
 
