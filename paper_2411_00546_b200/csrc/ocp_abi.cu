@@ -1115,6 +1115,15 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out)
   if (!ctx || !fac || !v || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
+  if (ctx->fmt == 1) {   // one fused launch: rhs gathered per line, out[own] = x[own]
+    double bytes = 0;
+    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
+    Timer t(ctx, CLS_SOLVE, 0, bytes);
+    CK(launch_block_solve(3, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
+                          ctx->P.off, ctx->maxNPS, v, out, ctx->P.n));
+    ++ctx->launches;
+    return OCP_OK;
+  }
   k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, v, ctx->B);
   CKL();
   {

@@ -624,15 +624,24 @@ __device__ __forceinline__ double jvp_rhs(const SubInfo& s, const double* d, int
   return e;
 }
 
+// RAS-apply right-hand side: the global v restricted to local point t of line a
+__device__ __forceinline__ double ras_rhs(const SubInfo& s, const double* v, int gn, int a, int t) {
+  int i, j;
+  local_to_global(s, a, t >> 1, i, j);
+  return v[(long long)(t & 1) * gn * gn + (long long)i * gn + j];
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(BS_MAX_THREADS, 2)
 k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, const double* in_pool,
               double scale, double* out_pool, double off, int max_npb, const double* dglob,
               double* oglob, int gn) {
   // MODE 0: solve pool -> pool.  MODE 1: the backward sweep stops at the first
-  // owned line (JVP / RAS apply).  MODE 2: the fused JVP (schwarz.py:327-345):
-  // MODE 1 with the right-hand side A_ext d computed from the global d and
-  // out[own] = -(d + x)[own] written straight to the global vector.
+  // owned line.  MODE 2: the fused JVP (schwarz.py:327-345): MODE 1 with the
+  // right-hand side A_ext d computed from the global d and out[own] =
+  // -(d + x)[own] written straight to the global vector.  MODE 3: the fused
+  // RAS apply (schwarz.py:221-239): right-hand side v restricted to the
+  // rectangle, out[own] = x[own].
   extern __shared__ __align__(16) double sm[];
   const SubInfo s = subs[list[blockIdx.x]];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -661,7 +670,8 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
   }
   // line 0 input, stored permuted: vp[t ^ 1] = vin[t]
   for (int t = tid; t < NPS; t += blockDim.x)
-    vp[t ^ 1] = t < n ? (MODE == 2 ? jvp_rhs(s, dglob, gn, off, 0, t) : scale * in[t]) : 0.0;
+    vp[t ^ 1] = t < n ? (MODE == 2 ? jvp_rhs(s, dglob, gn, off, 0, t)
+                         : MODE == 3 ? ras_rhs(s, dglob, gn, 0, t) : scale * in[t]) : 0.0;
   __syncthreads();
   if (warp == (int)(blockDim.x >> 5) - 1) {
     // ---- producer: stage t = (line blk, k) into slot t % BS_STAGES
@@ -706,7 +716,9 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
     double nxt = 0.0;
     if (h == 0 && i < n) {
       if (fwd) {
-        if (a + 1 < nr) nxt = MODE == 2 ? jvp_rhs(s, dglob, gn, off, a + 1, i) : in[(long long)(a + 1) * n + i];
+        if (a + 1 < nr)
+          nxt = MODE == 2 ? jvp_rhs(s, dglob, gn, off, a + 1, i)
+                : MODE == 3 ? ras_rhs(s, dglob, gn, a + 1, i) : in[(long long)(a + 1) * n + i];
       } else {
         nxt = out[(long long)a * n + i];
       }
@@ -754,22 +766,22 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
         // w_a = y; next input = scale in_{a+1} - off w_a (the last line starts
         // the backward sweep with x_{nr-1} = w_{nr-1})
         const double w = i < n ? y : 0.0;
-        if (i < n && (MODE != 2 || a + 1 < nr)) out[(long long)a * n + i] = w;
+        if (i < n && (MODE < 2 || a + 1 < nr)) out[(long long)a * n + i] = w;
         vnext[i ^ 1] = (a + 1 < nr) ? (i < n ? fma(-off, w, scale * nxt) : 0.0) : w;
         x = w;
       } else {
         // x_a = w_a - off y ; next input = x_a
         x = i < n ? fma(-off, y, nxt) : 0.0;
-        if (MODE != 2 && i < n) out[(long long)a * n + i] = x;
+        if (MODE < 2 && i < n) out[(long long)a * n + i] = x;
         vnext[i ^ 1] = x;
       }
-      if (MODE == 2 && (!fwd || a + 1 == nr) && i < n) {
-        // out[own] = -(d_loc + x)[own]  (k_jvp_out's rounding)
+      if (MODE >= 2 && (!fwd || a + 1 == nr) && i < n) {
+        // out[own] = -(d_loc + x)[own] (JVP, k_jvp_out's rounding) or x[own] (RAS)
         int gi, gj;
         local_to_global(s, a, i >> 1, gi, gj);
         if (gi >= s.or0 && gi < s.or1 && gj >= s.oc0 && gj < s.oc1) {
           const long long g = (long long)(i & 1) * gn * gn + (long long)gi * gn + gj;
-          oglob[g] = -add(dglob[g], x);
+          oglob[g] = MODE == 2 ? -add(dglob[g], x) : x;
         }
       }
     }
@@ -794,8 +806,11 @@ cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInf
   else if (mode == 1)
     k_block_solve<1><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
                                              dglob, oglob, gn);
-  else
+  else if (mode == 2)
     k_block_solve<2><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
+                                             dglob, oglob, gn);
+  else
+    k_block_solve<3><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
                                              dglob, oglob, gn);
   return cudaGetLastError();
 }
@@ -808,7 +823,9 @@ cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes) {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_block_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_block_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  e = cudaFuncSetAttribute(k_block_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_block_solve<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
 }
 
 }  // namespace ocp
