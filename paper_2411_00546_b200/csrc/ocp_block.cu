@@ -13,30 +13,34 @@
 // P J is symmetric (P swaps the y / p unknowns of every point: J = [[K, B12],
 // [B21, K]] with K = A + diag(phi') symmetric and B12, B21 diagonal), so
 // J^T = P J P, every Schur complement keeps S_a^T = P S_a P, and
-// W_a = S_a^{-1} P is symmetric.  The factor store keeps, per line, only the
-// upper triangle of 16x16 tiles of W_a (NPS = round16(n), identity on the
-// padding), tile column by tile column, each column-major: 55 of 100 tiles at
-// NPS = 160, so a solve streams 55 % of the bytes of the full inverse.  The
-// factor runs the recursion on the transposes, S_a^T = D_a^T - off^2
-// (S_{a-1}^{-1})^T, so shared row i of its result is column i of S_a^{-1},
-// and column j of W_a is the head of shared row j^1.
+// W_a = S_a^{-1} P = M_a^{-1} with M_a = P S_a symmetric.  The factor store
+// keeps, per line, -W_a as the upper triangle of 16x16 tiles (NPS =
+// round16(n), identity on the padding; layout in ocp_kernels.cuh): 55 of 100
+// tiles at NPS = 160.
 //
-// k_block_factor: one CTA per subdomain; S stays resident in shared memory
-// (NPB <= 160; larger blocks use a per-CTA global scratch, L2-resident) and is
-// inverted in place by blocked Gauss-Jordan with 32-wide pivot panels:
-//     P1  Pinv = P^{-1} of the 32x32 pivot block (one warp, registers)
-//     P2  S[p, j] = Pinv S[p, j]                       (DMMA, row block)
-//     P3a S[i, j] -= S[i, p] S[p, j]     i, j not in p (DMMA, rank-32)
-//     P3b S[i, p] = -S[i, p] Pinv                      (DMMA, column block)
-// P3b of panel p runs concurrently with P1 of panel p+1.  Every flop except
-// the 32x32 pivot inverses is a DMMA (mma.sync.m8n8k4.f64) on shared-memory
-// operands; nothing round-trips through L2 (the band kernel's bottleneck).
+// k_block_factor: one persistent CTA per SM (12 warps) takes subdomains from
+// a cost-sorted queue; M stays resident in shared memory (NPB <= 160; larger
+// blocks keep their last rows in a per-CTA global scratch, L2-resident).  Per
+// line the E phase writes the previous line's -W to the store from the rows
+// it loads and rebuilds M_a = P D_a - off^2 P W_{a-1} P in place; then a
+// symmetric block sweep (Goodnight's sweep operator, 32-wide pivot panels,
+// result -M^{-1}) inverts it:
+//     P1  A^{-1} of the 32x32 pivot block (Gauss-Jordan, 2x2 pivots)
+//     P2  M[p, j] = A^{-1} M[p, j]                      (DMMA, row block)
+//     P3a M[i, j] -= M[i, p] M[p, j], upper tiles only (DMMA), mirrored
+//     P3b M[i, p] = M[p, i]^T, M[p, p] = -A^{-1}        (register transpose)
+// P1 of panel p+1 runs on warps 0..3 (lookahead) while the other warps finish
+// P3a and P3b of panel p; P1 of panel 0 runs under the E phase of rows 32+.
+// Every flop except the pivot inverses is a DMMA (mma.sync.m8n8k4.f64) on
+// shared-memory operands.
 //
-// k_block_solve<MODE>: one CTA per subdomain; the tile columns of W_a stream
-// through a ring of TMA bulk-copy stages; thread t accumulates output row t
-// from the stored tiles and every off-diagonal tile is applied a second time,
-// transposed, by 16-lane column reductions; MODE 1 (JVP / RAS apply) stops
-// the backward sweep at the first owned line (schwarz.py:344).
+// k_block_solve<MODE>: one CTA per subdomain, a producer warp streaming
+// tile-column pairs of each line through a ring of TMA bulk copies (+ an L2
+// prefetch of the next line) and two consumer threads per row accumulating
+// the full symmetric row (stored tiles + the transposed column above the
+// diagonal tile).  MODE 0: inner-Newton solve (pool to pool); MODE 1: the
+// backward sweep stops at the first owned line (schwarz.py:344); MODE 2: the
+// fused JVP; MODE 3: the fused RAS apply.
 #include "ocp_kernels.cuh"
 #include "ocp_tma.cuh"
 
