@@ -102,12 +102,6 @@ __device__ __forceinline__ double d_entry(const SubInfo& s, const double* JL, in
   return 0.0;
 }
 
-// P1: in-place Gauss-Jordan inverse of the 32x32 block at S[p0.., p0..] by
-// one warp.  Lane j holds column j in registers; the rows are rotated by one
-// position per pivot step so that the pivot row is always c[0] - the pivot
-// loop stays a runtime loop (compact code) with no dynamic register indexing,
-// and nothing goes through memory between steps.  After 32 steps the
-// rotation is back to the identity.
 // reciprocal without the IEEE slow path (no call => nothing spills around
 // it): MUFU seed + two Newton steps, ~1 ulp; pivots are O(1/h^2) normals
 __device__ __forceinline__ double rcp64(double x) {
@@ -120,8 +114,8 @@ __device__ __forceinline__ double rcp64(double x) {
 }
 
 // P1: in-place Gauss-Jordan inverse of the 32x32 block at S[p0.., p0..] by
-// PW warps (named barrier 2).  Thread (w, lane) keeps rows 8w..8w+7 of
-// column `lane` in registers; every pivot step reads the pivot column / row
+// PW warps (named barrier 2).  Thread (w, lane) keeps rows R w .. R w + R - 1
+// (R = 32 / PW) of column `lane` in registers; every pivot step reads the pivot column / row
 // from one of two ping-pong 32x33 buffers and writes its updated entries to
 // the other, so a step costs one barrier.  No shuffles: inside a
 // warp-uniform branch the compiler wraps each shfl in a convergence check.
