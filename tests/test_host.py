@@ -182,3 +182,28 @@ def test_bench_replica_reduction_gloo_world2():
     assert out[0] == out[1]
     ms, tot, val = out[0]
     assert ms == 110.0 and tot == 3000.0 and val == pytest.approx(3000.0 / 0.11)
+
+
+def test_buffer_pools_retire_to_the_process_cache(monkeypatch):
+    """Engine teardown hands cached device buffers to the process-wide
+    retired cache (reused by size by the next engine, bounded, thread-safe);
+    nothing here touches a device: _raw_free is replaced by a recorder."""
+    from paper_2411_00546_b200 import _native as nat
+    freed = []
+    monkeypatch.setattr(nat, "_raw_free", lambda addr: freed.append(addr))
+    monkeypatch.setattr(nat, "_RETIRED", nat._RetiredCache(limit_bytes=3 << 20))
+    a = nat.BufferPool()
+    a.give(0x1000, 1 << 20)
+    a.give(0x2000, 1 << 20)
+    a.give(0x3000, 2 << 20)
+    a.release_all()                      # engine A torn down (its stream idle)
+    assert freed == [0x3000] and nat._RETIRED.cached == 2 << 20   # the 2 MB one exceeds the limit
+    b = nat.BufferPool()
+    got = b.take(1 << 20)                # engine B reuses a retired buffer of that size
+    assert got in (0x1000, 0x2000)
+    assert b.take(5 << 20) is None       # no buffer of that size: caller allocates
+    nat._RETIRED.give(0x4000, 4 << 20)   # over the cache limit: freed at once
+    assert 0x4000 in freed
+    nat.empty_cache()
+    assert nat._RETIRED.cached == 0
+    assert sorted(freed) == sorted([0x3000, 0x4000, 0x1000 if got == 0x2000 else 0x2000])
