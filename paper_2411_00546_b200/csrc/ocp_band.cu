@@ -356,11 +356,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       //          triangles of the factor store:
       //            L11^-1 = [[La^-1, 0], [X, Lc^-1]],  X = -Lc^-1 L_ba La^-1
       //            U11^-1 = [[Ua^-1, Y], [0, Uc^-1]],  Y = -Ua^-1 U_ab Uc^-1
-#ifndef OCP_EXP_NO_INV
       if (warp == SIDE) {
-#else
-      if (false) {
-#endif
         double* Lb = fac + (long long)K * 2 * NBF * LD;
         double* Ub = Lb + NBF * LD;
         const int j = lane & 15;
@@ -485,11 +481,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
             for (int ni = 0; ni < 2; ++ni)
               if (mi < mrows)
                 *reinterpret_cast<double2*>(win + addr[mi][ni]) = make_double2(c[mi][ni][0], c[mi][ni][1]);
-#ifndef OCP_EXP_NO_LA
           if (warp == LAW && wt == 0 && K + 1 < nblk) {
-#else
-          if (false) {
-#endif
             // tile 0 holds the next panel's A_aa (rows/cols [k0+32, k0+48)),
             // now final: factor it here, overlapped with the other warps' update
             __syncwarp();
@@ -518,9 +510,7 @@ k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P_, const doub
       }
       __syncthreads();
       PHASE_MARK(6);
-#ifndef OCP_EXP_IGNORE_BAD
       if (bad) break;
-#endif
       ks += NBF;
       ks -= ks >= WS ? WS : 0;
     }
