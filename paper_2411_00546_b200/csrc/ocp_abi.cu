@@ -57,6 +57,7 @@ struct ocp_ctx {
   double *d_alpha = nullptr, *d_norm2 = nullptr, *d_rpart = nullptr;
   unsigned int* d_rcount = nullptr;
   int res_chunks = 1;
+  int res_smem = 0;           // dynamic shared memory of k_residual
   long long* d_bad = nullptr;
   double* scratch = nullptr;
   long long ws_stride = 0;
@@ -216,9 +217,9 @@ int launch_residual(ocp_ctx* ctx, const int* d_list, int cnt, const double* x, c
   // (48 B per local point: read y,p,f,y_d, write r1,r2 - SURVEY.md 8d)
   Timer t(cnt == ctx->I && !D ? ctx : nullptr, CLS_RESID, 0, ctx->resid_bytes_all);
   const dim3 grid(cnt, ctx->res_chunks);
-  k_residual<<<grid, 256, 0, ctx->stream>>>(ctx->d_subs, d_list, ctx->P, x, V, D, alpha, ctx->d_f,
-                                             ctx->d_yd, eps, R, ctx->d_norm2, ctx->d_rpart,
-                                             ctx->d_rcount);
+  k_residual<<<grid, RES_THREADS, ctx->res_smem, ctx->stream>>>(
+      ctx->d_subs, d_list, ctx->P, x, V, D, alpha, ctx->d_f, ctx->d_yd, eps, R, ctx->d_norm2,
+      ctx->d_rpart, ctx->d_rcount);
   CKL();
   return OCP_OK;
 }
@@ -467,10 +468,16 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(cudaMalloc(&ctx->d_alpha, I * sizeof(double)));
   CKC(cudaMalloc(&ctx->d_norm2, I * sizeof(double)));
   {
-    // residual grid: one CTA per 32x32 tile of the oriented local grid
-    int maxt = 1;
-    for (auto& sub : ctx->subs) maxt = std::max(maxt, ((sub.nr + 31) / 32) * ((sub.nc + 31) / 32));
+    // residual grid: one CTA per RQ consecutive local points, staging the
+    // points plus one local row either side in dynamic shared memory
+    int maxt = 1, max_nc = 1;
+    for (auto& sub : ctx->subs) {
+      maxt = std::max(maxt, (sub.nr * sub.nc + RQ - 1) / RQ);
+      max_nc = std::max(max_nc, sub.nc);
+    }
     ctx->res_chunks = maxt;
+    ctx->res_smem = (int)residual_smem_bytes(max_nc);
+    CKC(cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->res_smem));
   }
   CKC(cudaMalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
   CKC(cudaMalloc(&ctx->d_rcount, I * sizeof(unsigned int)));

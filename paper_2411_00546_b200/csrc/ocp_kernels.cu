@@ -81,23 +81,128 @@ __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const dou
 // local residual (+ squared norm) of the listed subdomains at V + alpha_i D
 // _local_problem.local_residual (schwarz.py:181-186); R may be null (trial)
 // ---------------------------------------------------------------------------
-// Shared-memory halo tiles: a CTA owns a 32x32 tile of the oriented local
-// grid.  The (v + alpha d) tile plus its 1-point halo is staged in shared
-// memory with loads coalesced in local (band) order; the points are then
-// evaluated with threads running fast along the GLOBAL column index, so the
-// f / y_d / exterior-ring reads are coalesced for both orientations; the
-// residual tile goes back through shared memory to be stored in local order.
-constexpr int RT = 32;   // tile edge (oriented points)
+// A CTA owns RQ = 1024 consecutive local points q of one subdomain (flat
+// band order q = a * nc + b), 4 per thread.  The (v + alpha d) values of
+// q in [base - nc, base + RQ + nc) - the CTA's points plus one local row of
+// halo on either side - are staged in shared memory with contiguous,
+// coalesced loads (alpha d added once per element); the five stencil
+// entries of a point are then the staged values at q, q -+ 1, q -+ nc.
+// Every lane of a CTA but the last of a subdomain is busy (no 2D tile
+// padding), and the per-point index work is one division by nc.  f / y_d
+// are read at the point's global index (coalesced for orient 0, per-lane
+// strided rows for orient 1) before the staging barrier; the residual is
+// stored at q (coalesced).
+template <int OR>
+__device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
+                                                const double* __restrict__ x,
+                                                const double2* __restrict__ V,
+                                                const double2* __restrict__ D, double al,
+                                                const double* __restrict__ f,
+                                                const double* __restrict__ yd, double eps,
+                                                double2* __restrict__ R, int base, double2* tv) {
+  constexpr int PPT = RQ / RES_THREADS;
+  const int nr = s.nr, nc = s.nc, n = P.n, real = nr * nc;
+  const long long Ntot = (long long)n * n;
+  const int lo = base - nc;
+  // 0. this thread's points: oriented coordinates, f / y_d loads in flight
+  int la[PPT], lb[PPT];
+  double fv[PPT], ydv[PPT];
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const int q = base + threadIdx.x + RES_THREADS * u;
+    la[u] = q / nc;
+    lb[u] = q - la[u] * nc;
+    fv[u] = ydv[u] = 0.0;
+    if (q < real) {
+      const long long g = OR == 0 ? (long long)(s.r0 + la[u]) * n + (s.c0 + lb[u])
+                                  : (long long)(s.r0 + lb[u]) * n + (s.c0 + la[u]);
+      fv[u] = f[g];
+      ydv[u] = yd[g];
+    }
+  }
+  // 1. stage v + alpha d (newton.py:106: product rounded first)
+  const int cnt = RQ + 2 * nc;
+  for (int e = threadIdx.x; e < cnt; e += RES_THREADS) {
+    const int q = lo + e;
+    double2 v = make_double2(0.0, 0.0);
+    if (q >= 0 && q < real) {
+      v = V[q];
+      if (D) {
+        const double2 d = D[q];
+        v.x = add(v.x, mul(al, d.x));
+        v.y = add(v.y, mul(al, d.y));
+      }
+    }
+    tv[e] = v;
+  }
+  __syncthreads();
+  // 2. evaluate
+  double acc = 0.0;
+#pragma unroll
+  for (int u = 0; u < PPT; ++u) {
+    const int q = base + threadIdx.x + RES_THREADS * u;
+    if (q >= real) continue;
+    const double2* c = tv + (q - lo);
+    const double2 cv = c[0];
+    const bool in_u = la[u] > 0, in_d = la[u] < nr - 1, in_l = lb[u] > 0, in_r = lb[u] < nc - 1;
+    // the four neighbours in ascending global column order (csr_matvec):
+    // (i-1,j), (i,j-1), (i,j+1), (i+1,j)
+    double2 nv[4];
+    bool in[4];
+    if (OR == 0) {
+      nv[0] = c[-nc]; nv[1] = c[-1]; nv[2] = c[1]; nv[3] = c[nc];
+      in[0] = in_u; in[1] = in_l; in[2] = in_r; in[3] = in_d;
+    } else {
+      nv[0] = c[-1]; nv[1] = c[-nc]; nv[2] = c[nc]; nv[3] = c[1];
+      in[0] = in_l; in[1] = in_u; in[2] = in_d; in[3] = in_r;
+    }
+    // local part from the staged values, exterior part from the frozen
+    // global iterate; off * 0.0 = -0.0 and s + -0.0 == s bitwise for every s,
+    // so an absent entry contributes exactly nothing
+    double sly = 0.0, slp = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (t == 2) {
+        sly = add(sly, mul(P.diag, cv.x));
+        slp = add(slp, mul(P.diag, cv.y));
+      }
+      sly = add(sly, mul(P.off, in[t] ? nv[t].x : 0.0));
+      slp = add(slp, mul(P.off, in[t] ? nv[t].y : 0.0));
+    }
+    double sey = 0.0, sep = 0.0;
+    if (!(in[0] && in[1] && in[2] && in[3])) {
+      const int i = OR == 0 ? s.r0 + la[u] : s.r0 + lb[u];
+      const int j = OR == 0 ? s.c0 + lb[u] : s.c0 + la[u];
+      const int di[4] = {-1, 0, 0, 1};
+      const int dj[4] = {0, -1, 1, 0};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int ii = i + di[t], jj = j + dj[t];
+        if (in[t] || ii < 0 || ii >= n || jj < 0 || jj >= n) continue;
+        const long long g = (long long)ii * n + jj;
+        sey = add(sey, mul(P.off, x[g]));
+        sep = add(sep, mul(P.off, x[Ntot + g]));
+      }
+    }
+    const double ay = add(sly, sey), ap = add(slp, sep);
+    double r1, r2;
+    residual_rows(P, ay, ap, cv.x, cv.y, fv[u], ydv[u], eps, r1, r2);
+    acc = fma(r1, r1, acc);
+    acc = fma(r2, r2, acc);
+    if (R) R[q] = make_double2(r1, r2);
+  }
+  return acc;
+}
 
-__global__ void __launch_bounds__(256, 4) k_residual(const SubInfo* subs, const int* list, Phys P,
-                                                  const double* x, const double* Vpool,
-                                                  const double* Dpool, const double* alpha,
-                                                  const double* f, const double* yd, double eps,
-                                                  double* Rpool, double* norm2, double* partials,
-                                                  unsigned int* counters) {
-  __shared__ double2 tv[(RT + 2) * (RT + 2)];   // halo tile of v + alpha d, [a+1][b+1];
-                                                // reused for the residual tile [a][b] (+1 pad)
-  double2* tr = tv;
+size_t residual_smem_bytes(int max_nc) { return (size_t)(RQ + 2 * max_nc) * sizeof(double2); }
+
+__global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const SubInfo* subs, const int* list, Phys P,
+                                                      const double* x, const double* Vpool,
+                                                      const double* Dpool, const double* alpha,
+                                                      const double* f, const double* yd, double eps,
+                                                      double* Rpool, double* norm2, double* partials,
+                                                      unsigned int* counters) {
+  extern __shared__ double2 tv[];
   __shared__ double red[32];
   __shared__ bool is_last;
   const int sid = list[blockIdx.x];
@@ -106,143 +211,13 @@ __global__ void __launch_bounds__(256, 4) k_residual(const SubInfo* subs, const 
   const double2* D = Dpool ? reinterpret_cast<const double2*>(Dpool + s.loc) : nullptr;
   double2* R = Rpool ? reinterpret_cast<double2*>(Rpool + s.loc) : nullptr;
   const double al = alpha ? alpha[sid] : 0.0;
-  const long long Ntot = (long long)P.n * P.n;
-  const int tb_n = (s.nc + RT - 1) / RT;
-  const int tile = blockIdx.y;
-  const int a0 = (tile / tb_n) * RT, b0 = (tile % tb_n) * RT;
+  const int base = blockIdx.y * RQ;
   double acc = 0.0;
-  if (a0 < s.nr) {
-    const int lane = threadIdx.x & 31, row = threadIdx.x >> 5;
-    const int n = P.n;
-    // 0. issue this thread's f / y_d loads first (independent of the tile)
-    double fv[RT / 8], ydv[RT / 8];
-#pragma unroll
-    for (int u = 0; u < RT / 8; ++u) {
-      const int k = row + 8 * u;
-      const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
-      const int la = a0 + ta, lb = b0 + tbb;
-      fv[u] = ydv[u] = 0.0;
-      if (la < s.nr && lb < s.nc) {
-        int i, j;
-        local_to_global(s, la, lb, i, j);
-        const long long g = (long long)i * n + j;
-        fv[u] = f[g];
-        ydv[u] = yd[g];
-      }
-    }
-    // 1. stage the halo tile (local order, coalesced along b); all loads of
-    //    this thread are issued before the first use (latency overlap)
-    {
-      constexpr int HALO = (RT + 2) * (RT + 2);
-      constexpr int PER = (HALO + 255) / 256;
-      double2 hv[PER], hd[PER];
-      unsigned inmask = 0u;
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int e = threadIdx.x + 256 * u;
-        const int ta = e / (RT + 2), tbb = e - ta * (RT + 2);
-        const int la = a0 + ta - 1, lb = b0 + tbb - 1;
-        const bool in = e < HALO && la >= 0 && la < s.nr && lb >= 0 && lb < s.nc;
-        inmask |= in ? (1u << u) : 0u;
-        hv[u] = in ? V[la * s.nc + lb] : make_double2(0.0, 0.0);
-        hd[u] = (in && D) ? D[la * s.nc + lb] : make_double2(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < PER; ++u) {
-        const int e = threadIdx.x + 256 * u;
-        if (e < HALO) {
-          double2 v = hv[u];
-          if (D && (inmask >> u & 1u)) {
-            v.x = add(v.x, mul(al, hd[u].x));
-            v.y = add(v.y, mul(al, hd[u].y));
-          }
-          tv[e] = v;
-        }
-      }
-    }
-    __syncthreads();
-    // 2. evaluate, threads fast along the global column
-    double2 res[RT / 8];
-#pragma unroll
-    for (int u = 0; u < RT / 8; ++u) {
-      res[u] = make_double2(0.0, 0.0);
-      const int k = row + 8 * u;
-      // orient 0: global column = b -> (a, b) = (k, lane); orient 1: column = a -> (lane, k)
-      const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
-      const int la = a0 + ta, lb = b0 + tbb;
-      if (la >= s.nr || lb >= s.nc) continue;
-      int i, j;
-      local_to_global(s, la, lb, i, j);
-      // neighbours in ascending global column order (csr_matvec), local part
-      // from the tile, exterior part from the frozen global iterate
-      double sly = 0.0, slp = 0.0, sey = 0.0, sep = 0.0;
-      const double2* c = tv + (ta + 1) * (RT + 2) + tbb + 1;
-      if (la > 0 && la < s.nr - 1 && lb > 0 && lb < s.nc - 1) {
-        // interior of the rectangle: all five entries are local; tile
-        // offsets of (i-1,j), (i,j-1), (i,j+1), (i+1,j) for this orientation
-        const int o1 = s.orient == 0 ? -(RT + 2) : -1;
-        const int o2 = s.orient == 0 ? -1 : -(RT + 2);
-        const double2 v1 = c[o1], v2 = c[o2], v3 = c[0], v4 = c[-o2], v5 = c[-o1];
-        sly = add(0.0, mul(P.off, v1.x));   // csr_matvec starts its sum at 0.0
-        slp = add(0.0, mul(P.off, v1.y));
-        sly = add(sly, mul(P.off, v2.x));
-        slp = add(slp, mul(P.off, v2.y));
-        sly = add(sly, mul(P.diag, v3.x));
-        slp = add(slp, mul(P.diag, v3.y));
-        sly = add(sly, mul(P.off, v4.x));
-        slp = add(slp, mul(P.off, v4.y));
-        sly = add(sly, mul(P.off, v5.x));
-        slp = add(slp, mul(P.off, v5.y));
-        sly = add(sly, 0.0);   // the empty exterior part (csr sum of no terms is 0.0)
-        slp = add(slp, 0.0);
-      } else {
-        const int di[5] = {-1, 0, 0, 0, 1};
-        const int dj[5] = {0, -1, 0, 1, 0};
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-          const int ii = i + di[t], jj = j + dj[t];
-          if (ii < 0 || ii >= n || jj < 0 || jj >= n) continue;
-          const double coef = (t == 2) ? P.diag : P.off;
-          if (in_rect(s, ii, jj)) {
-            // oriented offsets of the neighbour inside the tile (+1 halo)
-            const int na = s.orient == 0 ? ii - s.r0 : jj - s.c0;
-            const int nbb = s.orient == 0 ? jj - s.c0 : ii - s.r0;
-            const double2 v = tv[(na - a0 + 1) * (RT + 2) + (nbb - b0 + 1)];
-            sly = add(sly, mul(coef, v.x));
-            slp = add(slp, mul(coef, v.y));
-          } else {
-            const long long g = (long long)ii * n + jj;
-            sey = add(sey, mul(coef, x[g]));
-            sep = add(sep, mul(coef, x[Ntot + g]));
-          }
-        }
-      }
-      const double ay = add(sly, sey), ap = add(slp, sep);
-      const double2 v = c[0];
-      double r1, r2;
-      residual_rows(P, ay, ap, v.x, v.y, fv[u], ydv[u], eps, r1, r2);
-      res[u] = make_double2(r1, r2);
-      acc = fma(r1, r1, acc);
-      acc = fma(r2, r2, acc);
-    }
-    // 3. residual tile back in local order (through the staging tile)
-    if (R) {
-      __syncthreads();
-#pragma unroll
-      for (int u = 0; u < RT / 8; ++u) {
-        const int k = row + 8 * u;
-        const int ta = s.orient == 0 ? k : lane, tbb = s.orient == 0 ? lane : k;
-        tr[ta * (RT + 1) + tbb] = res[u];
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < RT * RT; e += blockDim.x) {
-        const int ta = e / RT, tbb = e - ta * RT;
-        const int la = a0 + ta, lb = b0 + tbb;
-        if (la < s.nr && lb < s.nc) R[la * s.nc + lb] = tr[ta * (RT + 1) + tbb];
-      }
-    }
+  if (base < s.nr * s.nc) {
+    acc = s.orient == 0 ? residual_flat<0>(s, P, x, V, D, al, f, yd, eps, R, base, tv)
+                        : residual_flat<1>(s, P, x, V, D, al, f, yd, eps, R, base, tv);
   }
-  const double tot = block_sum<256>(acc, red);
+  const double tot = block_sum<RES_THREADS>(acc, red);
   if (threadIdx.x == 0) {
     partials[(long long)sid * gridDim.y + blockIdx.y] = tot;
     __threadfence();

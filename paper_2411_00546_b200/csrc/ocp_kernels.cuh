@@ -2,9 +2,24 @@
 #pragma once
 #include "ocp_common.cuh"
 
+// local residual: RQ flat local points per CTA of RES_THREADS threads, min
+// resident CTAs per SM
+#ifndef OCP_RES_THREADS
+#define OCP_RES_THREADS 256
+#endif
+#ifndef OCP_RES_PPT
+#define OCP_RES_PPT 4
+#endif
+constexpr int RES_THREADS = OCP_RES_THREADS;
+constexpr int RQ = OCP_RES_THREADS * OCP_RES_PPT;
+#ifndef OCP_RES_MINB
+#define OCP_RES_MINB 4
+#endif
+
 namespace ocp {
 
 __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const double* x, double* pool);
+size_t residual_smem_bytes(int max_nc);
 __global__ void k_residual(const SubInfo* subs, const int* list, Phys P, const double* x,
                            const double* Vpool, const double* Dpool, const double* alpha,
                            const double* f, const double* yd, double eps, double* Rpool,

@@ -33,9 +33,16 @@ for l in dis[start + 1:]:
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.split("\n")))
-hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
-i_s = hdr.index("Warp Stall Sampling (All Samples)")
+hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+hdr = rows[hi]
+data = []
+for r in rows[hi + 1:]:
+    if not r or r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
+col = os.environ.get("NCU_COL", "Warp Stall Sampling (All Samples)")
+i_s = hdr.index(col)
 base = int(data[0][0], 16)
 a2l = dict(ins)
 byline = collections.Counter()
