@@ -64,6 +64,29 @@ def test_local_residual_matches_oracle(case):
         np.testing.assert_allclose(r, ref, rtol=0, atol=4e-16 * scale * 4)
 
 
+@pytest.mark.parametrize("n,s1,s2,m", [(127, 2, 3, 4), (150, 3, 2, 6), (63, 1, 1, 0)])
+def test_local_residual_multi_chunk_bitwise(n, s1, s2, m):
+    """Subdomains of several 1024-point residual CTAs (halo rows crossing CTA
+    boundaries, both orientations, a 1x1 decomposition with no exterior):
+    bitwise equal to the oracle's frozen-exterior local residual
+    (schwarz.py:174-186) for the cubic phi."""
+    phi, nu, mu, eps = make_phi("cubic"), 1e-3, 1e-2, 1e-2
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, s1, s2, m)
+    eng = build_local_systems(dec, spec)
+    prob = O.Problem(n, s1, s2, m, phi, nu, mu, spec.f, spec.y_d)
+    rng = np.random.default_rng(7 + n)
+    x = 0.3 * rng.standard_normal(2 * n * n)
+    v = np.concatenate([x[s.pair_idx] + 0.01 for s in dec.subdomains])
+    assert max(s.size for s in dec.subdomains) > 1024
+    xd, vd, rd = eng.from_host(x), eng.from_host(v), eng.vector(v.shape[0])
+    eng.check(eng.lib.ocp_local_residual(eng.ctx, xd.ptr, vd.ptr, eps, rd.ptr), "res")
+    offs = np.cumsum([0] + [2 * s.size for s in dec.subdomains])
+    ref = np.concatenate([prob.local_fns(i, x)[0](v[offs[i]:offs[i + 1]], eps)
+                          for i in range(len(dec.subdomains))])
+    np.testing.assert_array_equal(rd.to_host(), ref)
+
+
 @pytest.mark.parametrize("case", UNIT_CASES, ids=IDS)
 def test_local_direction_matches_superlu(case):
     import scipy.sparse.linalg as spla

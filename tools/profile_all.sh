@@ -23,3 +23,8 @@ ncu --set full --import-source on --clock-control none --kernel-name-base demang
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k "regex:k_arnoldi_lag" -s 3 -c 1 -o gpurun_out/r1_arnoldi \
     python tools/arnoldi_bench.py 140 > gpurun_out/ncu3.log 2>&1
+# local-residual stencil: full capture of one full-set launch (x = 0)
+python tools/resid_bench.py cfg4 5 > gpurun_out/rb.log
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+    -k "regex:k_residual" -s 0 -c 1 -o gpurun_out/r1_resid \
+    python tools/profile_cfg4.py cfg4 1 > gpurun_out/ncu4.log 2>&1
