@@ -323,6 +323,13 @@ def run_ours(args):
     if traffic:
         roofline["traffic_source"] = traffic["source"]
 
+    stress = None
+    if not args.no_stress:
+        try:
+            stress = {name: stress_config5(name) for name in ("cfg5", "cfg5u")}
+        except Exception as exc:   # reported, never fatal to the headline line
+            stress = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(sample=16)
@@ -352,10 +359,69 @@ def run_ours(args):
                 "definition": "DOF-updates / whole e2e solve time (conservative vs value)"},
         "gpu_launches": int(st["launches"]),
         "clocks": clocks,
+        "stress_config5": stress,
     }
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     dist.close()
+
+
+def stress_config5(name, reps=3):
+    """BASELINE config 5 (batched-kernel stress test): one RAS sweep at x = 0
+    (eps fixed at 1e-3, inner tol 1e-8) plus one JVP with d ~ N(0,1) seed 1,
+    CUDA-event timed on the context stream after one untimed warm-up.  The
+    reference's own CPU times for the same sweep + JVP come from the golden
+    fixture's record (tests/golden/make_golden.py run_sweep)."""
+    from paper_2411_00546_b200 import ContinuationSchedule, NewtonConfig, build_local_systems, decompose
+    from paper_2411_00546_b200.problems import CONFIGS, build_spec
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep
+
+    cfg = CONFIGS[name]
+    spec = build_spec(cfg, with_matrix=False)
+    dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    eng = build_local_systems(dec, spec)
+    x = eng.from_host(np.zeros(cfg.unknowns))
+    fac = eng.factor_store()
+    sched = ContinuationSchedule.fixed(cfg.eps_min)
+    inner = NewtonConfig(tol=1e-8, max_outer=200)
+    d = eng.from_host(np.random.default_rng(1).standard_normal(cfg.unknowns))
+    fval, out = eng.vector(), eng.vector(cfg.unknowns)   # outputs allocated outside the timed region
+    _sweep(eng, x, fac, sched, inner, fval)
+    _jvp(eng, fac, d, out)
+    eng.sync()
+    eng.set_profiling(True)
+    eng.reset_stats()
+    sweep_ms, jvp_ms = [], []
+    for _ in range(reps):
+        eng.mark(2)
+        fval, iters = _sweep(eng, x, fac, sched, inner, fval)
+        eng.mark(3)
+        out = _jvp(eng, fac, d, out)
+        eng.mark(4)
+        eng.sync()
+        sweep_ms.append(eng.elapsed_ms(2, 3))
+        jvp_ms.append(eng.elapsed_ms(3, 4))
+    st = eng.stats()
+    sw, jv = statistics.mean(sweep_ms), statistics.mean(jvp_ms)
+    res = {"workload": f"BASELINE config 5 ({name}): {cfg.n}x{cfg.n} grid, {cfg.s1}x{cfg.s2} subdomains, "
+                       f"overlap {cfg.overlap}, eps fixed {cfg.eps_min:g}; one raspen_residual(x=0) + one "
+                       "raspen_jacobian_apply(d ~ N(0,1), seed 1)",
+           "sweep_ms": sw, "jvp_ms": jv, "sweep_plus_jvp_ms": sw + jv,
+           "inner_iters": sorted(set(int(i) for i in iters)),
+           "dof_updates_per_s": st["dof_updates"] / reps / (sw / 1e3),
+           "factor_tflops": st["factor_flops"] / st["factor_ms"] / 1e9 if st["factor_ms"] else None,
+           "jvp_solve_gbs": st["solve_bytes"] / st["solve_ms"] / 1e6 if st["solve_ms"] else None,
+           "fval_norm": fval.norm(), "jvp_norm": out.norm()}
+    gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", f"{name}_sweep.npz")
+    if os.path.exists(gpath):
+        g = np.load(gpath)
+        res["reference_cpu"] = {"sweep_s": float(g["sweep_wall"]), "jvp_s": float(g["jvp_wall"]),
+                                "threads": int(g["threads"]),
+                                "where": "build container, unmodified reference (golden run)"}
+    dec.__dict__.get("_engines", {}).clear()
+    del eng, x, fac, d, fval, out
+    gc.collect()
+    return res
 
 
 def cpu_baseline(sample, threads=None):
@@ -421,6 +487,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stress", action="store_true", help="skip the config-5 stress timing")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
