@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -76,6 +77,7 @@ struct ocp_ctx {
   double* arn_partials = nullptr;          // [2][2048] block partials of the Arnoldi kernel
   unsigned long long arn_epoch = 0;        // arrivals so far on arn_bar
   double* gm_Q = nullptr;      // persistent GMRES basis (grow-only), ocp_raspen_gmres
+  long long gm_n = 0;          // vector length the basis columns were sized for
   double* gm_w = nullptr;
   long long gm_cols = 0;
   double* gm_dh = nullptr;     // two device slots of Arnoldi coefficients (pipelined GMRES)
@@ -113,6 +115,31 @@ struct ocp_ctx {
 };
 
 namespace {
+
+// The GMRES basis of a destroyed context (stream-ordered pool memory, its
+// stream idle) is kept for the next context of the process: a fresh context
+// of the same problem size then solves without growing a multi-GB basis by
+// doubling (each growth a new pool block + copy; fragmented pool blocks made
+// some growths map new physical memory in the middle of a solve).
+std::mutex g_spare_mu;
+double* g_spare_Q = nullptr;
+size_t g_spare_bytes = 0;
+
+void spare_put(double* q, size_t bytes, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_spare_mu);
+  if (bytes > g_spare_bytes) std::swap(q, g_spare_Q), std::swap(bytes, g_spare_bytes);
+  if (q) cudaFreeAsync(q, st);
+}
+
+double* spare_take(size_t min_bytes, size_t* bytes) {
+  std::lock_guard<std::mutex> lk(g_spare_mu);
+  if (!g_spare_Q || g_spare_bytes < min_bytes) return nullptr;
+  double* q = g_spare_Q;
+  *bytes = g_spare_bytes;
+  g_spare_Q = nullptr;
+  g_spare_bytes = 0;
+  return q;
+}
 
 int fail(ocp_ctx* ctx, int code, const char* fmt, ...) {
   char buf[1024];
@@ -577,7 +604,9 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
 
 void ocp_ctx_destroy(ocp_ctx* ctx) {
   if (!ctx) return;
-  if (ctx->gm_Q && ctx->stream) cudaFreeAsync(ctx->gm_Q, ctx->stream);   // back to the memory pool
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->gm_Q && ctx->stream)   // kept for the next context (or back to the memory pool)
+    spare_put(ctx->gm_Q, (size_t)ctx->gm_cols * ctx->gm_n * sizeof(double), ctx->stream);
   ctx->gm_Q = nullptr;
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
@@ -1266,6 +1295,19 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
   // basis Q: the reference grows an (n, cap+1) array by doubling
   // (krylov.py:89-107); here one grow-only device buffer is kept by the
   // context (doubling too), so repeated solves do not reallocate
+  if (ctx->gm_Q && ctx->gm_n != n) {   // a basis for another vector length
+    cudaFreeAsync(ctx->gm_Q, st);
+    ctx->gm_Q = nullptr;
+    ctx->gm_cols = 0;
+  }
+  if (!ctx->gm_Q) {
+    size_t bytes = 0;
+    if (double* q = spare_take((size_t)(std::min(32, max_iters) + 2) * n * sizeof(double), &bytes)) {
+      ctx->gm_Q = q;
+      ctx->gm_cols = (long long)(bytes / ((size_t)n * sizeof(double)));
+    }
+  }
+  ctx->gm_n = n;
   auto ensure = [&](long long cols) -> bool {
     if (cols <= ctx->gm_cols) return true;
     long long ncols = std::max(cols, 2 * ctx->gm_cols);

@@ -1,7 +1,9 @@
 """Where the end-to-end raspen_solve time goes beyond the device solve (config 4),
 in bench.py's state (a device-resident engine stays alive): context build,
 x0 upload, device solve (wall vs CUDA-event sum), x download, GC pauses."""
+import cProfile
 import gc
+import pstats
 import sys
 import time
 
@@ -12,6 +14,7 @@ from paper_2411_00546_b200 import KrylovConfig, NewtonConfig, build_local_system
 from paper_2411_00546_b200.schwarz import solve_on_device  # noqa: E402
 from paper_2411_00546_b200.system import ProblemSpec  # noqa: E402
 
+prof = len(sys.argv) > 1 and sys.argv[1] == "profile"
 sys.argv = ["bench.py"]
 import bench  # noqa: E402
 
@@ -48,9 +51,15 @@ for rep in range(6):
     t2 = time.perf_counter()
     eng.set_profiling(True)
     eng.reset_stats()
+    if prof:
+        pr = cProfile.Profile()
+        pr.enable()
     x, r = solve_on_device(eng, x0d, sched, newton_cfg, kry, 1e-7, 200)
     eng.sync()
     t3 = time.perf_counter()
+    if prof:
+        pr.disable()
+        pstats.Stats(pr).sort_stats("tottime").print_stats(8)
     xh = x.to_host()
     t4 = time.perf_counter()
     st = eng.stats()
