@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const Su
   extern __shared__ double2 tv[];
   __shared__ double red[32];
   __shared__ bool is_last;
-  const int sid = list[blockIdx.x];
+  const int sid = list ? list[blockIdx.x] : blockIdx.x;   // null list: all subdomains
   const SubInfo s = subs[sid];
   const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
   const double2* D = Dpool ? reinterpret_cast<const double2*>(Dpool + s.loc) : nullptr;
