@@ -70,6 +70,7 @@ struct ocp_ctx {
   double* bscratch = nullptr;  // block format: global Schur blocks too large for shared memory
   long long bs_stride = 0;
   int bf_grid = 1;
+  bool bf_narrow = false;     // narrow-line factor instance (ocp_block_narrow.cu)
   int lu_grid = 1, num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
@@ -278,7 +279,7 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     auto cost = [&](int i) {
       const SubInfo& su = ctx->subs[i];
       const double c = (double)su.nr * su.pad_ * su.pad_ * su.pad_;
-      return su.pad_ > BF_SMEM_MAX_NPB ? 4.0 * c : c;
+      return su.pad_ > (ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB) ? 4.0 * c : c;
     };
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
     for (int i = 0; i < cnt; ++i) ctx->h_flist[i] = ord[i];
@@ -286,9 +287,14 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, (cnt + 1) * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
     const int grid = std::min(cnt, ctx->bf_grid);
-    k_block_factor<<<grid, block_factor_threads(), block_factor_smem_bytes(ctx->maxNPB), ctx->stream>>>(
-        ctx->d_subs, ctx->d_flist, cnt, ctx->P, ctx->JD, fac, ctx->bscratch, ctx->bs_stride,
-        ctx->d_status);
+    if (ctx->bf_narrow) {
+      CK(launch_narrow_factor(grid, ctx->stream, ctx->d_subs, ctx->d_flist, cnt, &ctx->P, ctx->JD,
+                              fac, ctx->bscratch, ctx->bs_stride, ctx->d_status));
+    } else {
+      k_block_factor<<<grid, block_factor_threads(), block_factor_smem_bytes(ctx->maxNPB),
+                       ctx->stream>>>(ctx->d_subs, ctx->d_flist, cnt, ctx->P, ctx->JD, fac,
+                                      ctx->bscratch, ctx->bs_stride, ctx->d_status);
+    }
     CKL();
     return OCP_OK;
   }
@@ -548,8 +554,18 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
     CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
   }
-  ctx->bf_grid = std::max(1, std::min(I, ctx->num_sms));
-  if (ctx->fmt == 1 && ctx->maxNPB > BF_SMEM_MAX_NPB) {
+  // narrow lines (config 5): a 6-warp factor CTA, two per SM, when there
+  // are enough subdomains to fill them and nearly every line fits its
+  // 96-unknown shared-memory block (ocp_block_narrow.cu)
+  if (ctx->fmt == 1 && I >= 2 * ctx->num_sms) {
+    int fit = 0;
+    for (auto& sub : ctx->subs) fit += sub.pad_ <= narrow_factor_max_npb();
+    ctx->bf_narrow = 10LL * fit >= 9LL * I;
+  }
+  const int bf_per_sm = ctx->bf_narrow ? narrow_factor_ctas_per_sm() : 1;
+  const int bf_max_npb = ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB;
+  ctx->bf_grid = std::max(1, std::min(I, bf_per_sm * ctx->num_sms));
+  if (ctx->fmt == 1 && ctx->maxNPB > bf_max_npb) {
     ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
     CKC(cudaMalloc(&ctx->bscratch, ctx->bf_grid * ctx->bs_stride * sizeof(double)));
   }
@@ -593,6 +609,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
         return cleanup_fail(OCP_ERR_UNSUPPORTED);
       }
       CKC(set_block_kernel_smem(fb, sb));
+      if (ctx->bf_narrow) CKC(narrow_set_factor_smem());
     }
   }
 #undef CKC

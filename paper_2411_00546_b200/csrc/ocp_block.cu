@@ -517,7 +517,10 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
   if (warp == 0) bulk_wait_all();
 }
 
-__global__ void __launch_bounds__(BF_THREADS, 1)
+#ifndef OCP_BF_MINB
+#define OCP_BF_MINB 1
+#endif
+__global__ void __launch_bounds__(BF_THREADS, OCP_BF_MINB)
 k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const double* JDpool,
                double* fac_pool, double* gscratch, long long gs_stride, int* status) {
   extern __shared__ __align__(16) double sm[];

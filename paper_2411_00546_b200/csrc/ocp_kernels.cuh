@@ -103,6 +103,13 @@ cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInf
                                double* out_pool, double off, int max_npb,
                                const double* dglob = nullptr, double* oglob = nullptr, int gn = 0);
 cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes);
+// narrow-line instance of the block factor (ocp_block_narrow.cu)
+int narrow_factor_max_npb();
+int narrow_factor_ctas_per_sm();
+cudaError_t narrow_set_factor_smem();
+cudaError_t launch_narrow_factor(int grid, cudaStream_t st, const SubInfo* subs, const int* list,
+                                 int cnt, const Phys* P, const double* JDpool, double* fac_pool,
+                                 double* scratch, long long ws_stride, int* status);
 // one full MGS Arnoldi step (ocp_krylov.cu); cudaErrorNotSupported if n too large
 cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const double* Q,
                            long long ldq, int j, const double* w_in, double* partials,
