@@ -28,3 +28,8 @@ python tools/resid_bench.py cfg4 5 > gpurun_out/rb.log
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k "regex:k_residual" -s 0 -c 1 -o gpurun_out/r1_resid \
     python tools/profile_cfg4.py cfg4 1 > gpurun_out/ncu4.log 2>&1
+# config-5 stress (narrow-line factor instance)
+python tools/stress_cfg5.py > gpurun_out/st.log
+ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
+    -k "regex:k_block_factor" -s 0 -c 1 -o gpurun_out/r1_factor_narrow \
+    python tools/stress_cfg5.py > gpurun_out/ncu5.log 2>&1
