@@ -324,7 +324,7 @@ def run_ours(args):
         roofline["traffic_source"] = traffic["source"]
 
     stress = None
-    if not args.no_stress:
+    if not args.no_stress and dist.ws == 1:   # single-GPU line only (a rank-local measurement)
         try:
             stress = {name: stress_config5(name) for name in ("cfg5", "cfg5u")}
         except Exception as exc:   # reported, never fatal to the headline line
