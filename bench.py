@@ -208,7 +208,7 @@ def run_ours(args):
     import torch
     torch.cuda.set_device(dist.local)
     from paper_2411_00546_b200 import KrylovConfig, NewtonConfig, build_local_systems, raspen_solve
-    from paper_2411_00546_b200.schwarz import solve_on_device
+    from paper_2411_00546_b200.schwarz import release_local_systems, solve_on_device
     from paper_2411_00546_b200.system import ProblemSpec
 
     cfg, spec, dec, sched = problem()
@@ -266,7 +266,7 @@ def run_ours(args):
             print(f"e2e step {it}: {(time.perf_counter() - t0) * 1e3:.1f} ms"
                   + (" (warm-up)" if it == 0 else ""), file=sys.stderr, flush=True)
             assert rep.converged, rep.failure
-            dec.__dict__.get("_engines", {}).pop(id(fresh), None)
+            release_local_systems(dec, fresh)
             del fresh, x
             gc.collect()   # outside the timed region: the step's engine is torn down now
     e2e_step = dist.max(statistics.mean(e2e_ms)) if e2e_ms else None
@@ -374,7 +374,7 @@ def stress_config5(name, reps=3):
     fixture's record (tests/golden/make_golden.py run_sweep)."""
     from paper_2411_00546_b200 import ContinuationSchedule, NewtonConfig, build_local_systems, decompose
     from paper_2411_00546_b200.problems import CONFIGS, build_spec
-    from paper_2411_00546_b200.schwarz import _jvp, _sweep
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep, release_local_systems
 
     cfg = CONFIGS[name]
     spec = build_spec(cfg, with_matrix=False)
@@ -418,7 +418,7 @@ def stress_config5(name, reps=3):
         res["reference_cpu"] = {"sweep_s": float(g["sweep_wall"]), "jvp_s": float(g["jvp_wall"]),
                                 "threads": int(g["threads"]),
                                 "where": "build container, unmodified reference (golden run)"}
-    dec.__dict__.get("_engines", {}).clear()
+    release_local_systems(dec)
     del eng, x, fac, d, fval, out
     gc.collect()
     return res

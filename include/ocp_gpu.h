@@ -92,6 +92,26 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x_dev, double* fac_dev,
                         int max_halvings, double* fval_dev,
                         int* inner_iters_host, int* failed_sub_host);
 
+/* ocp_raspen_residual with the refactorisation at `eps` instead of the
+ * inner schedule's floor: raspen_residual(x, dec, spec, eps, inner_cfg,
+ * inner_sched) solves the local problems along inner_sched and factors the
+ * local Jacobians at eps (schwarz.py:296-315). */
+int ocp_raspen_residual_at(ocp_ctx* ctx, const double* x_dev, double* fac_dev, double eps,
+                           double eps0, double gamma, double eps_min,
+                           double inner_tol, int inner_max_outer, double sigma,
+                           int max_halvings, double* fval_dev,
+                           int* inner_iters_host, int* failed_sub_host);
+
+/* Inner Newton of subdomain `sub` alone (local_correction, schwarz.py:211-218):
+ * only that subdomain is solved, so another subdomain's failure cannot
+ * surface.  Its values are then read with ocp_local_values; fac_dev is the
+ * scratch factor store of the inner solves (no refactorisation at the values,
+ * no f_val).  inner_iters_host[sub] receives its count. */
+int ocp_local_correction(ocp_ctx* ctx, const double* x_dev, double* fac_dev, int sub,
+                         double eps0, double gamma, double eps_min,
+                         double inner_tol, int inner_max_outer, double sigma,
+                         int max_halvings, int* inner_iters_host, int* failed_sub_host);
+
 /* Jacobian action from the stored factors of the last ocp_raspen_residual
  * into fac_dev: out[own_i] = -(d_loc + J_i^{-1} A_ext d)[own_i].
  * Replaces raspen_jacobian_apply (schwarz.py:327-345). */

@@ -17,6 +17,7 @@ from .newton import (ContinuationSchedule, LinearSolveError, LineSearchError, Ne
 from .krylov import GmresBreakdownError, GmresResult, KrylovConfig, gmres
 from .schwarz import (CorrectionSet, Decomposition, LocalSolveError, Subdomain,
                       build_local_systems, decompose, local_correction, ras_fixed_point_step,
+                      release_local_systems,
                       raspen_jacobian_apply, raspen_residual, raspen_solve)
 from .engine import DeviceVector, Engine
 from ._native import NativeError, NativeUnavailable

@@ -46,6 +46,9 @@ SIGNATURES = {
     "ocp_memset0": [_vp, _vp, ctypes.c_size_t],
     "ocp_sync": [_vp],
     "ocp_raspen_residual": [_vp, _vp, _vp, _d, _d, _d, _d, _i, _d, _i, _vp, _c_int_p, _c_int_p],
+    "ocp_raspen_residual_at": [_vp, _vp, _vp, _d, _d, _d, _d, _d, _i, _d, _i, _vp, _c_int_p,
+                               _c_int_p],
+    "ocp_local_correction": [_vp, _vp, _vp, _i, _d, _d, _d, _d, _i, _d, _i, _c_int_p, _c_int_p],
     "ocp_raspen_jvp": [_vp, _vp, _vp, _vp],
     "ocp_local_values": [_vp, _vp],
     "ocp_local_residual": [_vp, _vp, _vp, _d, _vp],

@@ -718,11 +718,14 @@ int ocp_sync(ocp_ctx* ctx) {
 // ---------------------------------------------------------------------------
 // the RAS sweep (raspen_residual, schwarz.py:285-324)
 // ---------------------------------------------------------------------------
-int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0, double gamma,
-                        double eps_min, double tol, int max_outer, double sigma, int max_halvings,
-                        double* fval, int* inner_iters, int* failed_sub) {
+// The batched inner Newton of every subdomain in `only` (all when only < 0),
+// then - for the whole set - the refactorisation at eps_fac and f_val.
+static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac, double eps0,
+                      double gamma, double eps_min, double tol, int max_outer, double sigma,
+                      int max_halvings, double* fval, int* inner_iters, int* failed_sub, int only) {
   if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
-  if (!ctx || !x || !fac || !fval) return fail(ctx, OCP_ERR_ARG, "null argument");
+  if (!ctx || !x || !fac || (only < 0 && !fval)) return fail(ctx, OCP_ERR_ARG, "null argument");
+  if (only >= ctx->I) return fail(ctx, OCP_ERR_ARG, "subdomain %d out of range", only);
   const int I = ctx->I;
   cudaStream_t st = ctx->stream;
   Timer sweep_timer(ctx, CLS_SWEEP);
@@ -748,6 +751,10 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
   CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int i = 0; i < I; ++i) {
+    if (only >= 0 && i != only) {   // local_correction: subdomain `only` alone
+      state[i] = DONE;
+      continue;
+    }
     nrm[i] = std::sqrt(ctx->h_norm2[i]);
     if (!std::isfinite(nrm[i])) {
       mark_fail(i, OCP_ERR_NONFINITE_INIT, "nonfinite residual at the initial guess");
@@ -852,10 +859,11 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
     return fail(ctx, why[lowest].code, "%s", why[lowest].msg.c_str());
   }
   if (failed_sub) *failed_sub = -1;
-  // refactorisation at the converged values (schwarz.py:305-315)
+  if (only >= 0) return OCP_OK;
+  // refactorisation at the converged values, at eps (schwarz.py:305-315)
   std::vector<int> all(I);
   for (int i = 0; i < I; ++i) all[i] = i;
-  k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->V, eps_min, ctx->JD,
+  k_jacdiag<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, ctx->V, eps_fac, ctx->JD,
                                ctx->d_bad);
   CKL();
   if (int rc = launch_factor(ctx, ctx->d_list_all, all, fac)) return rc;
@@ -881,6 +889,28 @@ int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0,
     }
   }
   return OCP_OK;
+}
+
+int ocp_raspen_residual(ocp_ctx* ctx, const double* x, double* fac, double eps0, double gamma,
+                        double eps_min, double tol, int max_outer, double sigma, int max_halvings,
+                        double* fval, int* inner_iters, int* failed_sub) {
+  return sweep_impl(ctx, x, fac, eps_min, eps0, gamma, eps_min, tol, max_outer, sigma, max_halvings,
+                    fval, inner_iters, failed_sub, -1);
+}
+
+int ocp_raspen_residual_at(ocp_ctx* ctx, const double* x, double* fac, double eps, double eps0,
+                           double gamma, double eps_min, double tol, int max_outer, double sigma,
+                           int max_halvings, double* fval, int* inner_iters, int* failed_sub) {
+  return sweep_impl(ctx, x, fac, eps, eps0, gamma, eps_min, tol, max_outer, sigma, max_halvings,
+                    fval, inner_iters, failed_sub, -1);
+}
+
+int ocp_local_correction(ocp_ctx* ctx, const double* x, double* fac, int sub, double eps0,
+                         double gamma, double eps_min, double tol, int max_outer, double sigma,
+                         int max_halvings, int* inner_iters, int* failed_sub) {
+  if (sub < 0) return fail(ctx, OCP_ERR_ARG, "subdomain %d out of range", sub);
+  return sweep_impl(ctx, x, fac, eps_min, eps0, gamma, eps_min, tol, max_outer, sigma,
+                    max_halvings, nullptr, inner_iters, failed_sub, sub);
 }
 
 int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out) {
@@ -1252,6 +1282,7 @@ int ocp_state_cg(ocp_ctx* ctx, const double* y, const double* b, double rel_tol,
   const double thr2 = rel_tol * rel_tol * bb;
   *iters_out = 0; *resid_out = std::sqrt(bb); *conv_out = 1;
   if (bb == 0.0) return OCP_OK;
+  CK(cudaMemcpyAsync(ctx->st_sc + 4, &thr2, sizeof(double), cudaMemcpyHostToDevice, st));
   int it = 0;
   while (it < max_iters) {
     const int it0 = it;
@@ -1270,8 +1301,8 @@ int ocp_state_cg(ocp_ctx* ctx, const double* y, const double* b, double rel_tol,
     for (int k = it0; k < it; ++k) {
       const double rr = ctx->st_hhist[k];
       if (!std::isfinite(rr)) return fail(ctx, OCP_ERR_NONFINITE, "CG residual@%d", k);
-      if (rr <= thr2) {
-        *iters_out = it; *resid_out = std::sqrt(ctx->st_hhist[it - 1]);
+      if (rr <= thr2) {   // the kernels froze x at this iterate
+        *iters_out = k + 1; *resid_out = std::sqrt(rr);
         return OCP_OK;
       }
     }

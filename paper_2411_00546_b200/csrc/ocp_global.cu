@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_ap(Phys P, const double* __r
                                                        double* __restrict__ Ap, double* partials,
                                                        unsigned int* counter, double* sc) {
   __shared__ double red[32];
+  // converged (r.r <= thr2 in sc[4]): the host polls every CG_POLL iterations,
+  // so later iterations of the batch leave x, r, p and the scalars untouched
+  if (sc[0] <= sc[4]) return;
   const int n = P.n;
   const long long N = (long long)n * n;
   double acc = 0.0;
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(long long N, const double
                                                        double* partials, unsigned int* counter,
                                                        double* sc, double* hist, int it) {
   __shared__ double red[32];
+  if (sc[0] <= sc[4]) return;   // converged in an earlier iteration of the batch
   const double alpha = sc[2];
   double acc = 0.0;
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(RED_THREADS) k_cg_xr(long long N, const double
 
 __global__ void k_cg_p(long long N, const double* __restrict__ r, double* __restrict__ p,
                        const double* sc) {
+  if (sc[0] <= sc[4]) return;   // converged: p is not needed again
   const double beta = sc[3];
   for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < N;
        k += (long long)gridDim.x * blockDim.x)

@@ -118,22 +118,39 @@ def decompose(grid, s1, s2, m):
 # device local systems
 # ---------------------------------------------------------------------------
 
+ENGINE_CACHE_SIZE = 2   # engines kept per decomposition (most recently used problems)
+
+
 def build_local_systems(dec, spec):
     """Device-side local systems of (dec, spec): the native engine (`schwarz.py:144-163`).
 
     The reference slices CSR blocks a_loc / a_ext; the device applies the same
     stencil matrix-free, so "building" means uploading f, y_d and the
-    subdomain table once.  Cached on the decomposition per problem.
+    subdomain table once.  Engines are cached on the decomposition for the
+    ``ENGINE_CACHE_SIZE`` most recently used problems; older ones are dropped,
+    which frees their device memory (a sweep over many ProblemSpecs does not
+    accumulate contexts).  An engine serialises its calls on one CUDA stream
+    and shares its scratch buffers between calls: it is not safe to use the
+    same (dec, spec) from several Python threads at once.
     """
-    cache = dec.__dict__.setdefault("_engines", {})
-    hit = cache.get(id(spec))
-    if hit is not None and hit[0] is spec:
-        return hit[1]
+    cache = dec.__dict__.setdefault("_engines", [])
+    for k, (s, eng) in enumerate(cache):
+        if s is spec:
+            cache.append(cache.pop(k))   # most recently used last
+            return eng
     eng = Engine(spec, dec.s1, dec.s2, dec.overlap)
     if eng.num_subdomains != len(dec):
         raise ValueError("decomposition does not match the native tiling")
-    cache[id(spec)] = (spec, eng)
+    cache.append((spec, eng))
+    while len(cache) > ENGINE_CACHE_SIZE:
+        cache.pop(0)
     return eng
+
+
+def release_local_systems(dec, spec=None):
+    """Drop the cached engine of ``spec`` (all engines when None) from ``dec``."""
+    cache = dec.__dict__.get("_engines", [])
+    cache[:] = [] if spec is None else [(s, e) for s, e in cache if s is not spec]
 
 
 def _engine(dec, spec, systems):
@@ -152,17 +169,25 @@ def _raise_native(engine, rc, failed):
     raise nat.NativeError(rc, msg, "ocp_raspen_residual")
 
 
-def _sweep(engine, x, fac, sched, inner_cfg, fval=None):
-    """One batched RAS sweep on device vectors -> (f_val, per-subdomain inner iterations)."""
+def _sweep(engine, x, fac, sched, inner_cfg, fval=None, eps=None):
+    """One batched RAS sweep on device vectors -> (f_val, per-subdomain inner iterations).
+
+    The local Jacobians are refactored at ``eps`` (default: the schedule's
+    floor, the only case raspen_solve produces), `schwarz.py:305-315`.
+    """
     fval = engine.vector() if fval is None else fval
     iters = np.zeros(engine.num_subdomains, dtype=np.int32)
     failed = np.zeros(1, dtype=np.int32)
     ip = iters.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int))
     fp = failed.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int))
-    rc = engine.lib.ocp_raspen_residual(
-        engine.ctx, x.ptr, nat.ctypes.c_void_p(fac.addr), float(sched.eps0), float(sched.gamma),
-        float(sched.eps_min), float(inner_cfg.tol), int(inner_cfg.max_outer),
-        float(inner_cfg.sigma), int(inner_cfg.max_halvings), fval.ptr, ip, fp)
+    args = (float(sched.eps0), float(sched.gamma), float(sched.eps_min), float(inner_cfg.tol),
+            int(inner_cfg.max_outer), float(inner_cfg.sigma), int(inner_cfg.max_halvings),
+            fval.ptr, ip, fp)
+    facp = nat.ctypes.c_void_p(fac.addr)
+    if eps is None or eps == sched.eps_min:
+        rc = engine.lib.ocp_raspen_residual(engine.ctx, x.ptr, facp, *args)
+    else:
+        rc = engine.lib.ocp_raspen_residual_at(engine.ctx, x.ptr, facp, float(eps), *args)
     if rc != nat.OCP_OK:
         _raise_native(engine, rc, int(failed[0]))
     return fval, [int(k) for k in iters]
@@ -203,15 +228,20 @@ def raspen_residual(x, dec, spec, eps, inner_cfg=None, inner_sched=None, threads
     engine = _engine(dec, spec, systems)
     cfg = inner_cfg if inner_cfg is not None else NewtonConfig(tol=1e-8)
     sched = inner_sched if inner_sched is not None else ContinuationSchedule.fixed(eps)
-    if sched.eps_min != eps:
-        # the device refactorises at the schedule's floor; the reference's
-        # callers always pass a schedule ending at eps (schwarz.py:372-375)
-        raise ValueError("inner schedule must end at eps")
     x = np.asarray(x, dtype=float)
     xd = engine.from_host(x)
     fac = engine.factor_store()
-    fval_d, inner = _sweep(engine, xd, fac, sched, cfg)
+    fval_d, inner = _sweep(engine, xd, fac, sched, cfg, eps=eps)
     f_val = fval_d.to_host()
+    values = _local_values(engine, dec)
+    _token_counter[0] += 1
+    return f_val, CorrectionSet(token=_token_counter[0], x=x.copy(), eps=eps, f_val=f_val,
+                                values=values, jac_locs=_LocalJacobians(dec, spec, values, eps), lus=fac,
+                                inner_iters=inner, systems=engine)
+
+
+def _local_values(engine, dec):
+    """Current local values of every subdomain, reference layout (host copies)."""
     flat = engine.vector(engine.ref_len)
     engine.check(engine.lib.ocp_local_values(engine.ctx, flat.ptr), "ocp_local_values")
     flat_h = flat.to_host()
@@ -219,10 +249,57 @@ def raspen_residual(x, dec, spec, eps, inner_cfg=None, inner_sched=None, threads
     for sub in dec.subdomains:
         values.append(flat_h[off:off + 2 * sub.size].copy())
         off += 2 * sub.size
-    _token_counter[0] += 1
-    return f_val, CorrectionSet(token=_token_counter[0], x=x.copy(), eps=eps, f_val=f_val,
-                                values=values, jac_locs=None, lus=fac, inner_iters=inner,
-                                systems=engine)
+    return values
+
+
+class _LocalJacobians:
+    """``CorrectionSet.jac_locs`` (`schwarz.py:321`): the local Jacobians at the values.
+
+    The device path never assembles them - their diagonals are regenerated
+    inside the factor kernel and only the factor store (``lus``) is kept - so
+    entry i is built on the host on first access, exactly as
+    `_local_pair_jacobian` builds it (`schwarz.py:166-171`): CSR
+    ``[[A_loc + diag(phi'(y)), diag(b12)], [diag(b21), A_loc + diag(phi'(y))]]``
+    at the local values and eps.  Inspection only; the JVP does not use it.
+    """
+
+    def __init__(self, dec, spec, values, eps):
+        self.dec, self.spec, self.values, self.eps = dec, spec, values, eps
+        self._cache = {}
+
+    def __len__(self):
+        return len(self.values)
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
+
+    def __getitem__(self, i):
+        if i < 0:
+            i += len(self)
+        if i not in self._cache:
+            self._cache[i] = _assemble_local_jacobian(self.dec.subdomains[i], self.spec,
+                                                      self.values[i], self.eps)
+        return self._cache[i]
+
+
+def _assemble_local_jacobian(sub, spec, v, eps):
+    import scipy.sparse as sp
+    from .system import smoothed_projection_derivative
+    rows = sub.rows[1] - sub.rows[0]
+    cols = sub.cols[1] - sub.cols[0]
+    size = rows * cols
+    h2 = spec.grid.h ** 2
+    t_r = sp.diags([np.full(rows - 1, -1.0), np.full(rows, 2.0), np.full(rows - 1, -1.0)],
+                   [-1, 0, 1])
+    t_c = sp.diags([np.full(cols - 1, -1.0), np.full(cols, 2.0), np.full(cols - 1, -1.0)],
+                   [-1, 0, 1])
+    a_loc = ((sp.kron(t_r, sp.identity(cols)) + sp.kron(sp.identity(rows), t_c)) / h2).tocsr()
+    y, p = v[:size], v[size:]
+    dphi = spec.phi.derivative(y)
+    b12 = (1.0 - smoothed_projection_derivative(-p / spec.mu, eps)) / spec.nu
+    b21 = spec.phi.second_derivative(y) * p - 1.0
+    a11 = a_loc + sp.diags(dphi)
+    return sp.bmat([[a11, sp.diags(b12)], [sp.diags(b21), a11]], format="csr")
 
 
 def raspen_jacobian_apply(x, d, dec, spec, eps, corrections):
@@ -242,13 +319,29 @@ def ras_fixed_point_step(x, dec, spec, eps, inner_cfg=None, inner_sched=None, th
 
 
 def local_correction(i, x, dec, spec, eps, inner_cfg=None, inner_sched=None, systems=None):
-    """Local values of subdomain i (`schwarz.py:211-218`).
+    """Local values solving the frozen-exterior system on subdomain i (`schwarz.py:211-218`).
 
-    The device solves every subdomain in one batch; a failure in any of them
-    surfaces here as that subdomain's LocalSolveError.
+    Only subdomain i is solved (``ocp_local_correction``), so a failure
+    elsewhere cannot surface here; its failure raises LocalSolveError(i).
     """
-    _, corr = raspen_residual(x, dec, spec, eps, inner_cfg, inner_sched, None, systems)
-    return corr.values[i]
+    engine = _engine(dec, spec, systems)
+    cfg = inner_cfg if inner_cfg is not None else NewtonConfig(tol=1e-8)
+    sched = inner_sched if inner_sched is not None else ContinuationSchedule.fixed(eps)
+    if not 0 <= i < len(dec):
+        raise IndexError(f"subdomain {i} out of range")
+    xd = engine.from_host(np.asarray(x, dtype=float))
+    iters = np.zeros(engine.num_subdomains, dtype=np.int32)
+    failed = np.zeros(1, dtype=np.int32)
+    fac = engine.factor_store()
+    rc = engine.lib.ocp_local_correction(
+        engine.ctx, xd.ptr, nat.ctypes.c_void_p(fac.addr), int(i), float(sched.eps0),
+        float(sched.gamma), float(sched.eps_min),
+        float(cfg.tol), int(cfg.max_outer), float(cfg.sigma), int(cfg.max_halvings),
+        iters.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int)),
+        failed.ctypes.data_as(nat.ctypes.POINTER(nat.ctypes.c_int)))
+    if rc != nat.OCP_OK:
+        _raise_native(engine, rc, int(failed[0]))
+    return _local_values(engine, dec)[i]
 
 
 def raspen_solve(x0, dec, spec, sched, cfg=None, krylov_cfg=None, inner_tol=1e-8,

@@ -62,6 +62,23 @@ def digest(v):
     }
 
 
+def support_bits(p, mu, eps):
+    """Full-grid control support of the reference solution, bit-packed.
+
+    `supp_bits`: |p| > mu, i.e. u != 0 of the unsmoothed projection
+    (`system.py:173-174` at eps -> 0); `band_bits`: ||p| - mu| <= eps, the
+    points where the north-star support criterion is waived.  One bit per
+    grid point, so the whole 1023^2 grid fits in ~2 x 131 KB before
+    compression.
+    """
+    p = np.asarray(p, dtype=float)
+    return {
+        "supp_bits": np.packbits(np.abs(p) > mu),
+        "band_bits": np.packbits(np.abs(np.abs(p) - mu) <= eps),
+        "supp_count": int(np.count_nonzero(np.abs(p) > mu)),
+    }
+
+
 def ref_spec(cfg):
     grid = RefGrid(cfg.n)
     f, y_d = build_fields(cfg)
@@ -135,6 +152,7 @@ def run_solve(name, inner_tol, threads, out_path):
     for key, vec in (("y", y), ("p", p), ("u", u)):
         for k, v in digest(vec).items():
             data[f"{key}_{k}"] = v
+    data.update(support_bits(p, cfg.mu, cfg.eps_min))
     np.savez_compressed(out_path, **data)
     print(f"{name} inner_tol={inner_tol}: converged={report.converged} "
           f"outer={report.outer_iters} inner={report.inner_iters} "
@@ -220,6 +238,77 @@ def run_units(out_path):
         data[f"{tag}_solve_per_sub"] = np.array(rec.per_eval(len(dec)))
         print(f"{tag}: inner={corr.inner_iters} solve outer={rep.outer_iters} "
               f"inner={rep.inner_iters} gmres={rep.gmres_iters} conv={rep.converged}")
+    np.savez_compressed(out_path, **data)
+
+
+def run_variants(out_path):
+    """Reference behaviour off the harness defaults (`schwarz.py:211-218,285-324,348-411`).
+
+    * ``raspen_solve(continuation=False)`` (`pkg/tests/test_schwarz.py:350-358`)
+      and ``raspen_solve(backtracking=True)`` (sigma 1.1 outer line search) on
+      the unit cases and on BASELINE config 1;
+    * ``raspen_residual`` with an inner schedule whose floor differs from eps
+      (solve with the schedule, refactor at eps: `schwarz.py:296-315`) and the
+      JVP from those stored factors;
+    * ``local_correction(i)`` of single subdomains (`schwarz.py:211-218`).
+    """
+    from paper_2411_00546_b200.problems import mild_spec
+
+    data = {}
+    cases = [
+        ("kappa16", 16, 2, 2, 2, Nonlinearity(0.1), 1e-2, 1.0),
+        ("cubic20", 20, 2, 3, 2, make_phi("cubic"), 1e-3, 1e-2),
+    ]
+    specs = []
+    for tag, n, s1, s2, m, phi, nu, mu in cases:
+        base = mild_spec(n)
+        grid = RefGrid(n)
+        spec = RefSpec(grid=grid, a=ref_laplacian(grid), phi=phi, nu=nu, mu=mu,
+                       f=base.f, y_d=10.0 * base.y_d)
+        specs.append((tag, spec, ref_schwarz.decompose(grid, s1, s2, m),
+                      ContinuationSchedule(1.0, 0.2, 1e-3)))
+    cfg = CONFIGS["cfg1"]
+    spec1 = ref_spec(cfg)
+    specs.append(("cfg1", spec1, ref_schwarz.decompose(spec1.grid, cfg.s1, cfg.s2, cfg.overlap),
+                  ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)))
+    for tag, spec, dec, sched in specs:
+        x0 = np.zeros(2 * spec.grid.size)
+        for var, kw in (("nocont", dict(continuation=False)),
+                        ("backtrack", dict(backtracking=True))):
+            with PerSubRecorder() as rec:
+                xs, rep = ref_schwarz.raspen_solve(
+                    x0, dec, spec, sched, cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+                    krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000), threads=1, **kw)
+            k = f"{tag}_{var}"
+            data[f"{k}_x"] = xs
+            data[f"{k}_converged"] = rep.converged
+            data[f"{k}_outer"] = rep.outer_iters
+            data[f"{k}_inner"] = np.array(rep.inner_iters)
+            data[f"{k}_gmres"] = np.array([-1 if g is None else g for g in rep.gmres_iters])
+            data[f"{k}_norms"] = np.array(rep.residual_norms)
+            data[f"{k}_alphas"] = np.array(rep.alphas)
+            data[f"{k}_per_sub"] = np.array(rec.per_eval(len(dec)))
+            print(f"{k}: conv={rep.converged} outer={rep.outer_iters} inner={rep.inner_iters} "
+                  f"gmres={rep.gmres_iters} alphas={rep.alphas}")
+        if tag == "cfg1":
+            continue
+        rng = np.random.default_rng(300 + spec.grid.n)
+        x = 0.3 * rng.standard_normal(2 * spec.grid.size)
+        d = rng.standard_normal(x.shape[0])
+        eps = 1e-2
+        # inner continuation to a floor below eps, then refactorisation at eps
+        f_val, corr = ref_schwarz.raspen_residual(
+            x, dec, spec, eps, inner_cfg=NewtonConfig(tol=1e-10),
+            inner_sched=ContinuationSchedule(1.0, 0.2, 1e-3), threads=1)
+        data[f"{tag}_floor_x"] = x
+        data[f"{tag}_floor_d"] = d
+        data[f"{tag}_floor_fval"] = f_val
+        data[f"{tag}_floor_inner"] = np.array(corr.inner_iters)
+        data[f"{tag}_floor_jvp"] = ref_schwarz.raspen_jacobian_apply(x, d, dec, spec, eps, corr)
+        for i in (0, len(dec) - 1):
+            data[f"{tag}_lc{i}"] = ref_schwarz.local_correction(
+                i, x, dec, spec, eps, inner_cfg=NewtonConfig(tol=1e-10))
+        print(f"{tag}: floor inner={corr.inner_iters}")
     np.savez_compressed(out_path, **data)
 
 
@@ -310,6 +399,7 @@ def run_ras_solve(name, out_path):
     for key, vec in (("y", y), ("p", p), ("u", u)):
         for k, v in digest(vec).items():
             data[f"{key}_{k}"] = v
+    data.update(support_bits(p, cfg.mu, cfg.eps_min))
     np.savez_compressed(out_path, **data)
     print(f"ras {name}: converged={report.converged} outer={report.outer_iters} "
           f"gmres={report.gmres_iters} alphas={report.alphas} failure={report.failure} "
@@ -368,6 +458,8 @@ def main():
         run_units(args.out or os.path.join(HERE, "units.npz"))
     elif args.what == "harness":
         run_harness(args.out or os.path.join(HERE, "harness.npz"))
+    elif args.what == "variants":
+        run_variants(args.out or os.path.join(HERE, "variants.npz"))
     elif args.what == "ras_units":
         run_ras_units(args.out or os.path.join(HERE, "ras_units.npz"))
     elif args.what.startswith("ras_cfg"):

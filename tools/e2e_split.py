@@ -11,7 +11,7 @@ import numpy as np
 
 sys.path.insert(0, ".")
 from paper_2411_00546_b200 import KrylovConfig, NewtonConfig, build_local_systems  # noqa: E402
-from paper_2411_00546_b200.schwarz import solve_on_device  # noqa: E402
+from paper_2411_00546_b200.schwarz import release_local_systems, solve_on_device  # noqa: E402
 from paper_2411_00546_b200.system import ProblemSpec  # noqa: E402
 
 prof = len(sys.argv) > 1 and sys.argv[1] == "profile"
@@ -66,6 +66,6 @@ for rep in range(6):
     dev = st["sweep_ms"] + st["jvp_ms"] + st["mgs_ms"]
     print(f"build {1e3*(t1-t0):.1f} upload {1e3*(t2-t1):.1f} solve {1e3*(t3-t2):.1f} (device {dev:.1f}) "
           f"download {1e3*(t4-t3):.1f} ms; gc {len(gc_ms)} pauses {sum(gc_ms):.1f} ms", flush=True)
-    dec.__dict__.get("_engines", {}).pop(id(fresh), None)
+    release_local_systems(dec, fresh)
     del fresh, eng, x, x0d
     gc.collect()
