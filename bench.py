@@ -330,9 +330,13 @@ def run_ours(args):
         except Exception as exc:   # reported, never fatal to the headline line
             stress = {"error": f"{type(exc).__name__}: {exc}"}
 
-    cpu = None
+    cpu = anchors = None
     if dist.rank == 0 and dist.ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(sample=16)
+        try:
+            anchors = cpu_anchors(stress)
+        except Exception as exc:   # reported, never fatal to the headline line
+            anchors = {"error": f"{type(exc).__name__}: {exc}"}
     rep = reps[-1]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.ws, "steps": args.steps,
@@ -360,6 +364,7 @@ def run_ours(args):
         "gpu_launches": int(st["launches"]),
         "clocks": clocks,
         "stress_config5": stress,
+        "cpu_anchors": anchors,
     }
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
@@ -412,16 +417,111 @@ def stress_config5(name, reps=3):
            "factor_tflops": st["factor_flops"] / st["factor_ms"] / 1e9 if st["factor_ms"] else None,
            "jvp_solve_gbs": st["solve_bytes"] / st["solve_ms"] / 1e6 if st["solve_ms"] else None,
            "fval_norm": fval.norm(), "jvp_norm": out.norm()}
-    gpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden", f"{name}_sweep.npz")
-    if os.path.exists(gpath):
-        g = np.load(gpath)
-        res["reference_cpu"] = {"sweep_s": float(g["sweep_wall"]), "jvp_s": float(g["jvp_wall"]),
-                                "threads": int(g["threads"]),
-                                "where": "build container, unmodified reference (golden run)"}
     release_local_systems(dec)
     del eng, x, fac, d, fval, out
     gc.collect()
     return res
+
+
+def blas_threads():
+    info = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS",
+                                           "MKL_NUM_THREADS")}
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{"api": d.get("internal_api"), "threads": d.get("num_threads")}
+                        for d in threadpool_info()]
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
+def cpu_anchors(stress):
+    """Same-box CPU anchors: the reference path (oracle port, same SuperLU /
+    sparsetools / BLAS calls as `pkg/src/ocp`) timed on this box's host cores
+    beside the GPU, on workloads small enough to finish in the bench.
+
+    * config 2, the whole raspen_solve (x = 0, harness settings) on the CPU
+      against the same whole solve through the GPU's public API (host arrays
+      in and out, context build included): the same quantity on both sides;
+    * config 5 uniform, one RAS sweep at x = 0 + one JVP on the CPU, against
+      the GPU's stress_config5 timing of the same pair.
+    """
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import raspen_oracle as O
+    from paper_2411_00546_b200 import (ContinuationSchedule, KrylovConfig, NewtonConfig,
+                                       decompose, raspen_solve)
+    from paper_2411_00546_b200.problems import CONFIGS, build_fields, build_spec
+    from paper_2411_00546_b200.schwarz import release_local_systems
+    from paper_2411_00546_b200.system import make_phi
+    cores = os.cpu_count() or 1
+    out = {"cores": cores, "kind": "port", "blas_threads": blas_threads(),
+           "cpu_model": _cpu_model()}
+    # config 2 whole solve
+    cfg = CONFIGS["cfg2"]
+    f, yd = build_fields(cfg)
+    prob = O.Problem(cfg.n, cfg.s1, cfg.s2, cfg.overlap, make_phi(cfg.phi), cfg.nu, cfg.mu, f, yd)
+    t0 = time.perf_counter()
+    xo, ro = O.raspen_solve(prob, np.zeros(cfg.unknowns), cfg.eps0, cfg.gamma, cfg.eps_min,
+                            inner_tol=1e-8, threads=cores)
+    cpu_s = time.perf_counter() - t0
+    dof = O.dof_updates(prob, ro["per_sub"])
+    spec = build_spec(cfg, with_matrix=False)
+    dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    sched = ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)
+    gpu_ms = []
+    for it in range(4):   # one warm-up, three timed, each on a fresh problem + context
+        fresh = type(spec)(grid=spec.grid, a=None, phi=spec.phi, nu=spec.nu, mu=spec.mu,
+                           f=spec.f.copy(), y_d=spec.y_d.copy())
+        t0 = time.perf_counter()
+        x, rep = raspen_solve(np.zeros(cfg.unknowns), dec, fresh, sched,
+                              cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+                              krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000),
+                              inner_tol=1e-8)
+        if it:
+            gpu_ms.append((time.perf_counter() - t0) * 1e3)
+        release_local_systems(dec, fresh)
+    gpu_s = statistics.mean(gpu_ms) / 1e3
+    out["cfg2_whole_solve"] = {
+        "workload": "BASELINE config 2 raspen_solve from x=0 (255^2, 4x4, overlap 8, inner tol 1e-8)",
+        "cpu_s": cpu_s, "gpu_e2e_s": gpu_s, "speedup": cpu_s / gpu_s,
+        "cpu_iterations": {"outer": ro["outer_iters"], "inner": ro["inner_iters"],
+                           "gmres": ro["gmres_iters"]},
+        "gpu_iterations": {"outer": rep.outer_iters, "inner": rep.inner_iters,
+                           "gmres": rep.gmres_iters},
+        "cpu_dof_updates_per_s_whole_solve": dof / cpu_s,
+        "gpu_dof_updates_per_s_whole_solve": dof / gpu_s,
+        "gpu_timer": "host perf_counter around the public raspen_solve (host arrays, context build)",
+    }
+    # config 5 uniform sweep + JVP
+    cfg = CONFIGS["cfg5u"]
+    f, yd = build_fields(cfg)
+    prob = O.Problem(cfg.n, cfg.s1, cfg.s2, cfg.overlap, make_phi(cfg.phi), cfg.nu, cfg.mu, f, yd)
+    x = np.zeros(cfg.unknowns)
+    t0 = time.perf_counter()
+    _, corr = O.raspen_residual(prob, x, cfg.eps_min, tol=1e-8, max_outer=200, threads=cores)
+    t1 = time.perf_counter()
+    d = np.random.default_rng(1).standard_normal(cfg.unknowns)
+    O.raspen_jvp(prob, x, d, cfg.eps_min, corr)
+    t2 = time.perf_counter()
+    rec = {"workload": "BASELINE config 5 uniform: one RAS sweep at x=0 (eps 1e-3) + one JVP",
+           "cpu_sweep_s": t1 - t0, "cpu_jvp_s": t2 - t1,
+           "note": "the reference's JVP loop is sequential by design (schwarz.py:14-15)"}
+    g = (stress or {}).get("cfg5u") if isinstance(stress, dict) else None
+    if g and "sweep_plus_jvp_ms" in g:
+        rec["gpu_sweep_plus_jvp_s"] = g["sweep_plus_jvp_ms"] / 1e3
+        rec["speedup"] = (t2 - t0) / rec["gpu_sweep_plus_jvp_s"]
+    out["cfg5u_sweep_jvp"] = rec
+    return out
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def cpu_baseline(sample, threads=None):
