@@ -232,6 +232,13 @@ int ocp_reset_stats(ocp_ctx* ctx);
 int ocp_event_record(ocp_ctx* ctx, int slot);
 int ocp_event_elapsed(ocp_ctx* ctx, int slot_a, int slot_b, double* ms_host);
 
+/* Verification aid (not on the hot path): with OCP_GUARD=1 in the
+ * environment every device buffer the library allocates carries 64 KB guard
+ * zones of a fill pattern on both sides; this counts guard bytes that kernels
+ * overwrote (out-of-bounds writes) across all live buffers.  OCP_ERR_ARG
+ * when guard zones are off. */
+int ocp_check_guards(long long* corrupted_bytes, long long* buffers);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,7 @@ SIGNATURES = {
     "ocp_stats": [_vp, _c_dbl_p, _i],
     "ocp_reset_stats": [_vp],
     "ocp_event_record": [_vp, _i],
+    "ocp_check_guards": [_c_ll_p, _c_ll_p],
     "ocp_event_elapsed": [_vp, _i, _i, _c_dbl_p],
 }
 _RESTYPES = {"ocp_ctx_destroy": None, "ocp_last_error": ctypes.c_char_p}

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -141,6 +142,82 @@ double* spare_take(size_t min_bytes, size_t* bytes) {
   g_spare_bytes = 0;
   return q;
 }
+
+// Guard-zone allocator (OCP_GUARD=1 in the environment): every device buffer
+// of the library gets GUARD_BYTES of a fill pattern on both sides, and
+// ocp_check_guards counts pattern bytes that kernels overwrote - an
+// out-of-bounds write detector that runs at full speed on any pool (the
+// GPU pool refuses compute-sanitizer).  The interior is filled with the same
+// pattern, so a read of never-written memory yields garbage, not zeros.
+constexpr size_t GUARD_BYTES = 64 << 10;
+constexpr unsigned char GUARD_FILL = 0xA5;
+std::mutex g_guard_mu;
+std::map<void*, std::pair<char*, size_t>> g_guards;   // user pointer -> (base, bytes)
+bool guard_on() {
+  static const bool on = [] {
+    const char* v = getenv("OCP_GUARD");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+cudaError_t guard_malloc(void** p, size_t bytes) {
+  if (!guard_on()) return cudaMalloc(p, bytes);
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, bytes + 2 * GUARD_BYTES);
+  if (e != cudaSuccess) return e;
+  e = cudaMemset(base, GUARD_FILL, bytes + 2 * GUARD_BYTES);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();   // before any non-blocking stream uses it
+  if (e != cudaSuccess) return e;
+  *p = base + GUARD_BYTES;
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guards[*p] = {base, bytes};
+  return cudaSuccess;
+}
+long long g_guard_freed_bad = 0;   // corrupted guard bytes of buffers already freed
+std::string g_guard_first;
+long long count_guard(const char* base, size_t bytes, std::string* first) {
+  std::vector<unsigned char> h(GUARD_BYTES);
+  long long bad = 0;
+  for (int side = 0; side < 2; ++side) {
+    const char* g = side ? base + GUARD_BYTES + bytes : base;
+    if (cudaMemcpy(h.data(), g, GUARD_BYTES, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (size_t k = 0; k < GUARD_BYTES; ++k)
+      if (h[k] != GUARD_FILL) {
+        if (first && first->empty()) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "buffer of %zu bytes: %s guard byte %zu overwritten", bytes,
+                   side ? "tail" : "head", k);
+          *first = buf;
+        }
+        ++bad;
+      }
+  }
+  return bad;
+}
+cudaError_t guard_free(void* p) {
+  if (!p) return cudaSuccess;
+  if (guard_on()) {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guards.find(p);
+    if (it != g_guards.end()) {
+      char* base = it->second.first;
+      cudaDeviceSynchronize();   // the buffer's last kernels have finished
+      const long long bad = count_guard(base, it->second.second, &g_guard_first);
+      if (bad > 0) g_guard_freed_bad += bad;
+      g_guards.erase(it);
+      return cudaFree(base);
+    }
+  }
+  return cudaFree(p);
+}
+template <class T>
+cudaError_t gmalloc(T** p, size_t bytes) {
+  void* v = nullptr;
+  const cudaError_t e = guard_malloc(&v, bytes);
+  *p = static_cast<T*>(v);
+  return e;
+}
+cudaError_t gfree(void* p) { return guard_free(p); }
 
 int fail(ocp_ctx* ctx, int code, const char* fmt, ...) {
   char buf[1024];
@@ -271,7 +348,7 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     // persistent CTAs take subdomains in list order: largest work first
     // (global-memory Schur blocks, then nr * NPB^3), so the tail is short
     if (!ctx->d_flist) {   // list + the work counter of the persistent CTAs
-      CK(cudaMalloc(&ctx->d_flist, (ctx->I + 1) * sizeof(int)));
+      CK(gmalloc(&ctx->d_flist, (ctx->I + 1) * sizeof(int)));
       CK(cudaMallocHost(&ctx->h_flist, (ctx->I + 1) * sizeof(int)));
     }
     CK(cudaStreamSynchronize(ctx->stream));   // h_flist may still feed a previous copy
@@ -483,25 +560,25 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     }
   }
   const int I = ctx->I;
-  CKC(cudaMalloc(&ctx->d_subs, I * sizeof(SubInfo)));
+  CKC(gmalloc(&ctx->d_subs, I * sizeof(SubInfo)));
   CKC(cudaMemcpy(ctx->d_subs, ctx->subs.data(), I * sizeof(SubInfo), cudaMemcpyHostToDevice));
   const size_t nbytes = ctx->N * sizeof(double);
-  CKC(cudaMalloc(&ctx->d_f, nbytes));
-  CKC(cudaMalloc(&ctx->d_yd, nbytes));
+  CKC(gmalloc(&ctx->d_f, nbytes));
+  CKC(gmalloc(&ctx->d_yd, nbytes));
   CKC(cudaMemcpy(ctx->d_f, f_host, nbytes, cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(ctx->d_yd, y_d_host, nbytes, cudaMemcpyHostToDevice));
   const size_t pbytes = ctx->pool_len * sizeof(double);
   for (double** p : {&ctx->V, &ctx->R, &ctx->D, &ctx->B}) {
-    CKC(cudaMalloc(p, pbytes));
+    CKC(gmalloc(p, pbytes));
     CKC(cudaMemset(*p, 0, pbytes));
   }
-  CKC(cudaMalloc(&ctx->JD, 2 * pbytes));
+  CKC(gmalloc(&ctx->JD, 2 * pbytes));
   CKC(cudaMemset(ctx->JD, 0, 2 * pbytes));
-  CKC(cudaMalloc(&ctx->d_list_all, I * sizeof(int)));
-  CKC(cudaMalloc(&ctx->d_list, I * sizeof(int)));
-  CKC(cudaMalloc(&ctx->d_status, I * sizeof(int)));
-  CKC(cudaMalloc(&ctx->d_alpha, I * sizeof(double)));
-  CKC(cudaMalloc(&ctx->d_norm2, I * sizeof(double)));
+  CKC(gmalloc(&ctx->d_list_all, I * sizeof(int)));
+  CKC(gmalloc(&ctx->d_list, I * sizeof(int)));
+  CKC(gmalloc(&ctx->d_status, I * sizeof(int)));
+  CKC(gmalloc(&ctx->d_alpha, I * sizeof(double)));
+  CKC(gmalloc(&ctx->d_norm2, I * sizeof(double)));
   {
     // residual grid: one CTA per RQ consecutive local points, staging the
     // points plus one local row either side in dynamic shared memory
@@ -512,13 +589,13 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     }
     ctx->res_chunks = maxt;
     ctx->res_smem = (int)residual_smem_bytes(max_nc);
-    CKC(cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, ctx->res_smem));
+    CKC(raise_smem_limit((const void*)k_residual, ctx->res_smem));
   }
-  CKC(cudaMalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
-  CKC(cudaMalloc(&ctx->d_rcount, I * sizeof(unsigned int)));
+  CKC(gmalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
+  CKC(gmalloc(&ctx->d_rcount, I * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->d_rcount, 0, I * sizeof(unsigned int)));
-  CKC(cudaMalloc(&ctx->d_bad, I * sizeof(long long)));
-  CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(int)));
+  CKC(gmalloc(&ctx->d_bad, I * sizeof(long long)));
+  CKC(gmalloc(&ctx->d_flags, 4 * sizeof(int)));
   {
     std::vector<int> all(I);
     for (int i = 0; i < I; ++i) all[i] = i;
@@ -541,7 +618,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       for (int k = 0; k < lo; ++k) sol[k] = ord[pos++];
       for (int k = hi; k < I; ++k) sol[k] = ord[pos++];
     }
-    CKC(cudaMalloc(&ctx->d_solve_order, I * sizeof(int)));
+    CKC(gmalloc(&ctx->d_solve_order, I * sizeof(int)));
     CKC(cudaMemcpy(ctx->d_solve_order, sol.data(), I * sizeof(int), cudaMemcpyHostToDevice));
   }
   // LU windows: up to 2 CTAs per SM, one (W+NB)^2 window each (L2 resident)
@@ -552,7 +629,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   }
   if (ctx->fmt == 0) {
     ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
-    CKC(cudaMalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
+    CKC(gmalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
   }
   // narrow lines (config 5): a 6-warp factor CTA, two per SM, when there
   // are enough subdomains to fill them and nearly every line fits its
@@ -567,17 +644,17 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->bf_grid = std::max(1, std::min(I, bf_per_sm * ctx->num_sms));
   if (ctx->fmt == 1 && ctx->maxNPB > bf_max_npb) {
     ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
-    CKC(cudaMalloc(&ctx->bscratch, ctx->bf_grid * ctx->bs_stride * sizeof(double)));
+    CKC(gmalloc(&ctx->bscratch, ctx->bf_grid * ctx->bs_stride * sizeof(double)));
   }
-  CKC(cudaMalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
-  CKC(cudaMalloc(&ctx->red_counter, sizeof(unsigned int)));
+  CKC(gmalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
+  CKC(gmalloc(&ctx->red_counter, sizeof(unsigned int)));
   CKC(cudaMemset(ctx->red_counter, 0, sizeof(unsigned int)));
-  CKC(cudaMalloc(&ctx->arn_bar, sizeof(unsigned long long)));
-  CKC(cudaMalloc(&ctx->arn_partials, 2 * 2048 * sizeof(double)));
+  CKC(gmalloc(&ctx->arn_bar, sizeof(unsigned long long)));
+  CKC(gmalloc(&ctx->arn_partials, 2 * 2048 * sizeof(double)));
   CKC(cudaMemset(ctx->arn_bar, 0, sizeof(unsigned long long)));
-  CKC(cudaMalloc(&ctx->d_result, 8 * sizeof(double)));
+  CKC(gmalloc(&ctx->d_result, 8 * sizeof(double)));
   ctx->h_cap = 4096;
-  CKC(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+  CKC(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_norm2, I * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_status, I * sizeof(int)));
   CKC(cudaMallocHost(&ctx->h_bad, I * sizeof(long long)));
@@ -594,8 +671,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
       return cleanup_fail(OCP_ERR_UNSUPPORTED);
     }
-    CKC(cudaFuncSetAttribute(k_band_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             factor_smem_bytes(ctx->maxW)));
+    CKC(raise_smem_limit((const void*)k_band_factor, factor_smem_bytes(ctx->maxW)));
     const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
     if (solve_smem > optin) {
       fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");
@@ -637,7 +713,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
                   (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist, (void*)ctx->d_solve_order,
                   (void*)ctx->d_h})
-    if (p) cudaFree(p);
+    if (p) gfree(p);
   for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
                   (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
                   (void*)ctx->gm_hh, (void*)ctx->st_hhist, (void*)ctx->h_flist})
@@ -678,13 +754,13 @@ int ocp_subdomain_table(const ocp_ctx* ctx, int* rects) {
 int ocp_malloc(size_t bytes, void** dev) {
   ocp_ctx* ctx = nullptr;
   if (!dev) return OCP_ERR_ARG;
-  CK(cudaMalloc(dev, std::max<size_t>(bytes, 16)));
+  CK(gmalloc(dev, std::max<size_t>(bytes, 16)));
   return OCP_OK;
 }
 
 int ocp_free(void* dev) {
   ocp_ctx* ctx = nullptr;
-  if (dev) CK(cudaFree(dev));
+  if (dev) CK(gfree(dev));
   return OCP_OK;
 }
 
@@ -968,7 +1044,7 @@ int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, doub
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
   double* fac = nullptr;
-  CK(cudaMalloc(&fac, ctx->fac_len * sizeof(double)));
+  CK(gmalloc(&fac, ctx->fac_len * sizeof(double)));
   k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
   CKL();
   if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->B, nullptr, nullptr, eps, ctx->D)) return rc;
@@ -983,7 +1059,7 @@ int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, doub
     CKL();
   }
   cudaStreamSynchronize(st);
-  cudaFree(fac);
+  gfree(fac);
   if (rc) return rc;
   CK(cudaMemcpy(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost));
   for (int i = 0; i < I; ++i)
@@ -1063,9 +1139,9 @@ int ocp_vec_all_finite(ocp_ctx* ctx, long long n, const double* x, int* finite) 
 int ocp_mgs(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int j, double* w, double* h_host) {
   if (j + 2 > ctx->h_cap) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaFree(ctx->d_h));
+    CK(gfree(ctx->d_h));
     ctx->h_cap = 2 * (j + 2);
-    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+    CK(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   }
   Timer t(ctx, CLS_MGS);
   cudaStream_t st = ctx->stream;
@@ -1088,9 +1164,9 @@ int ocp_arnoldi(ocp_ctx* ctx, long long n, double* Q, long long ldq, int j, cons
                 double* h_host) {
   if (j + 2 > ctx->h_cap) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaFree(ctx->d_h));
+    CK(gfree(ctx->d_h));
     ctx->h_cap = 2 * (j + 2);
-    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+    CK(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   }
   cudaStream_t st = ctx->stream;
   {
@@ -1138,7 +1214,7 @@ int ocp_global_residual(ocp_ctx* ctx, const double* x, double eps, double* r) {
 int ocp_global_jacobian(ocp_ctx* ctx, const double* x, double eps, double* jd) {
   if (!ctx || !x || !jd) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
-  if (!ctx->d_gbad) CK(cudaMalloc(&ctx->d_gbad, sizeof(unsigned long long)));
+  if (!ctx->d_gbad) CK(gmalloc(&ctx->d_gbad, sizeof(unsigned long long)));
   CK(cudaMemsetAsync(ctx->d_gbad, 0xff, sizeof(unsigned long long), st));
   k_global_jacdiag<<<ew_grid(ctx->N), 256, 0, st>>>(ctx->P, x, eps, reinterpret_cast<double4*>(jd),
                                                      ctx->d_gbad);
@@ -1250,19 +1326,19 @@ int ocp_state_cg(ocp_ctx* ctx, const double* y, const double* b, double rel_tol,
   cudaStream_t st = ctx->stream;
   const long long N = ctx->N;
   if (!ctx->st_buf) {
-    CK(cudaMalloc(&ctx->st_buf, 4 * (size_t)N * sizeof(double)));
-    CK(cudaMalloc(&ctx->st_sc, 8 * sizeof(double)));
+    CK(gmalloc(&ctx->st_buf, 4 * (size_t)N * sizeof(double)));
+    CK(gmalloc(&ctx->st_sc, 8 * sizeof(double)));
   }
   const int hcap = max_iters + CG_POLL;
   if (ctx->st_hcap < hcap) {
     cudaStreamSynchronize(st);
-    if (ctx->st_hist) cudaFree(ctx->st_hist);
+    if (ctx->st_hist) gfree(ctx->st_hist);
     if (ctx->st_hhist) cudaFreeHost(ctx->st_hhist);
-    CK(cudaMalloc(&ctx->st_hist, hcap * sizeof(double)));
+    CK(gmalloc(&ctx->st_hist, hcap * sizeof(double)));
     CK(cudaMallocHost(&ctx->st_hhist, hcap * sizeof(double)));
     ctx->st_hcap = hcap;
   }
-  if (!ctx->d_gbad) CK(cudaMalloc(&ctx->d_gbad, sizeof(unsigned long long)));
+  if (!ctx->d_gbad) CK(gmalloc(&ctx->d_gbad, sizeof(unsigned long long)));
   double *dg = ctx->st_buf, *r = dg + N, *p = r + N, *Ap = p + N;
   CK(cudaMemsetAsync(ctx->d_gbad, 0xff, sizeof(unsigned long long), st));
   k_state_diag<<<ew_grid(N), 256, 0, st>>>(ctx->P, y, dg, ctx->d_gbad);
@@ -1322,7 +1398,7 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
     return fail(ctx, OCP_ERR_ARG, "bad argument");
   cudaStream_t st = ctx->stream;
   const long long n = 2 * ctx->N;
-  if (kind == 1 && !ctx->gm_t && cudaMalloc(&ctx->gm_t, (size_t)n * sizeof(double)) != cudaSuccess)
+  if (kind == 1 && !ctx->gm_t && gmalloc(&ctx->gm_t, (size_t)n * sizeof(double)) != cudaSuccess)
     return fail(ctx, OCP_ERR_CUDA, "GMRES work vector allocation failed");
   const double* r0 = b;
   if (kind == 1) {   // mb = M b (krylov.py:55-60)
@@ -1368,16 +1444,16 @@ static int gmres_impl(ocp_ctx* ctx, int kind, const double* fac, const double* j
     ctx->gm_cols = ncols;
     return true;
   };
-  if (!ctx->gm_w && cudaMalloc(&ctx->gm_w, (size_t)n * sizeof(double)) != cudaSuccess)
+  if (!ctx->gm_w && gmalloc(&ctx->gm_w, (size_t)n * sizeof(double)) != cudaSuccess)
     return fail(ctx, OCP_ERR_CUDA, "GMRES work vector allocation failed");
   // Arnoldi coefficient slots: step j writes slot j&1 on the device, copies it
   // to pinned host memory and records gm_ev[j&1]
   if (ctx->gm_hcap < max_iters + 2) {
     cudaStreamSynchronize(st);
-    if (ctx->gm_dh) cudaFree(ctx->gm_dh);
+    if (ctx->gm_dh) gfree(ctx->gm_dh);
     if (ctx->gm_hh) cudaFreeHost(ctx->gm_hh);
     ctx->gm_dh = nullptr; ctx->gm_hh = nullptr; ctx->gm_hcap = 0;
-    if (cudaMalloc(&ctx->gm_dh, 2 * (size_t)(max_iters + 2) * sizeof(double)) != cudaSuccess ||
+    if (gmalloc(&ctx->gm_dh, 2 * (size_t)(max_iters + 2) * sizeof(double)) != cudaSuccess ||
         cudaMallocHost(&ctx->gm_hh, 2 * (size_t)(max_iters + 2) * sizeof(double)) != cudaSuccess)
       return fail(ctx, OCP_ERR_CUDA, "GMRES coefficient buffers");
     ctx->gm_hcap = max_iters + 2;
@@ -1517,9 +1593,9 @@ int ocp_gemv_add(ocp_ctx* ctx, long long n, const double* Q, long long ldq, int 
                  const double* x, double* out) {
   if (k + 2 > ctx->h_cap) {
     CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaFree(ctx->d_h));
+    CK(gfree(ctx->d_h));
     ctx->h_cap = 2 * (k + 2);
-    CK(cudaMalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
+    CK(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   }
   CK(cudaMemcpyAsync(ctx->d_h, y_host, k * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   k_gemv_add<<<ew_grid(n), 256, 0, ctx->stream>>>(n, Q, ldq, k, ctx->d_h, x, out);
@@ -1573,6 +1649,25 @@ int ocp_debug_phase(unsigned long long* out) {
   return 0;
 }
 #endif
+
+int ocp_check_guards(long long* corrupted, long long* buffers) {
+  ocp_ctx* ctx = nullptr;
+  if (!corrupted || !buffers) return fail(ctx, OCP_ERR_ARG, "null argument");
+  *corrupted = 0;
+  *buffers = 0;
+  if (!guard_on()) return fail(ctx, OCP_ERR_ARG, "guard zones are off (set OCP_GUARD=1)");
+  CK(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  *corrupted = g_guard_freed_bad;   // buffers freed so far were checked at free
+  for (const auto& kv : g_guards) {
+    const long long bad = count_guard(kv.second.first, kv.second.second, &g_guard_first);
+    if (bad < 0) return fail(ctx, OCP_ERR_CUDA, "guard readback failed");
+    *corrupted += bad;
+    ++*buffers;
+  }
+  if (*corrupted) g_global_err = g_guard_first;
+  return OCP_OK;
+}
 
 int ocp_event_record(ocp_ctx* ctx, int slot) {
   if (!ctx || slot < 0 || slot >= 16) return OCP_ERR_ARG;

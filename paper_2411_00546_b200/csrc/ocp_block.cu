@@ -817,16 +817,15 @@ cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInf
 }
 
 cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes) {
-  cudaError_t e = cudaFuncSetAttribute(k_block_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       factor_bytes);
+  cudaError_t e = raise_smem_limit((const void*)k_block_factor, factor_bytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_block_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  e = raise_smem_limit((const void*)k_block_solve<0>, solve_bytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_block_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  e = raise_smem_limit((const void*)k_block_solve<1>, solve_bytes);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_block_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  e = raise_smem_limit((const void*)k_block_solve<2>, solve_bytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_block_solve<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, solve_bytes);
+  return raise_smem_limit((const void*)k_block_solve<3>, solve_bytes);
 }
 
 }  // namespace ocp

@@ -27,8 +27,7 @@ int narrow_factor_max_npb() { return ocp_nw::BF_SMEM_MAX_NPB; }
 int narrow_factor_ctas_per_sm() { return OCP_BF_MINB; }
 
 cudaError_t narrow_set_factor_smem() {
-  return cudaFuncSetAttribute(ocp_nw::k_block_factor, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              ocp_nw::block_factor_smem_bytes(0));
+  return raise_smem_limit((const void*)ocp_nw::k_block_factor, ocp_nw::block_factor_smem_bytes(0));
 }
 
 cudaError_t launch_narrow_factor(int grid, cudaStream_t st, const SubInfo* subs, const int* list,

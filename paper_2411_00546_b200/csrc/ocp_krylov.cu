@@ -319,7 +319,7 @@ static cudaError_t launch_lag(cudaStream_t st, int grid, int per, long long n, c
                               double* h_out, unsigned long long* bar, unsigned long long* epoch) {
   void* fn = (void*)k_arnoldi_lag<CH>;
   const int smem = 2 * per * (int)sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_smem_limit((const void*)fn, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, LAG_THREADS, smem);
@@ -369,7 +369,7 @@ cudaError_t launch_arnoldi(cudaStream_t st, int num_sms, long long n, const doub
   else if (ch <= 32) { fn = (void*)k_arnoldi<32>; c = 32; }
   else return cudaErrorNotSupported;
   const int smem = c * ARN_THREADS * (int)sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = raise_smem_limit((const void*)fn, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ARN_THREADS, smem);

@@ -222,10 +222,9 @@ cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo
 }
 
 cudaError_t set_band_solve_smem(int bytes) {
-  cudaError_t e = cudaFuncSetAttribute(k_band_solve<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       bytes);
+  cudaError_t e = raise_smem_limit((const void*)k_band_solve<0>, bytes);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_band_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return raise_smem_limit((const void*)k_band_solve<1>, bytes);
 }
 
 }  // namespace ocp

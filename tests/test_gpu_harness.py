@@ -11,11 +11,12 @@ reproduces every artifact byte for byte apart from timing (`test_harness.py:167-
 """
 
 import json
+import os
 
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import REPO, golden
 from paper_2411_00546_b200.grid import Grid
 from paper_2411_00546_b200.harness import ExperimentConfig, read_field_csv, run_single
 from paper_2411_00546_b200.problem_setup import (construct_plateau_problem,
@@ -112,3 +113,20 @@ def test_run_single_deterministic_modulo_timing(tag, tmp_path):
     assert first == second
     for name in ("residual_history.csv", "y.csv", "p.csv", "u.csv"):
         assert (tmp_path / "a" / name).read_text() == (tmp_path / "b" / name).read_text()
+
+
+@pytest.mark.gpu
+def test_guard_zones_and_repeat_determinism():
+    """compute-sanitizer stand-in (the GPU pool refuses the sanitizer): every
+    device buffer carries 64 KB guard zones (OCP_GUARD=1) and no kernel of a
+    RASPEN, newton-ras-eps or CG run writes into them; repeated solves are
+    bitwise identical (races in the barrier / ticket / mbarrier code would
+    change bits).  tools/sanitize_run.py."""
+    import subprocess
+    import sys
+    env = dict(os.environ, OCP_GUARD="1", OCP_REPEAT="5")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sanitize_run.py"), "--all"],
+                         env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "corrupted_bytes=0" in out.stdout
+    assert "bitwise identical" in out.stdout

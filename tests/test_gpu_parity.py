@@ -510,3 +510,21 @@ def test_correction_set_jac_locs_are_the_local_jacobians():
         Jo = prob.local_fns(i, x)[1](corr.values[i], 1e-2)
         d = np.random.default_rng(i).standard_normal(J.shape[0])
         np.testing.assert_allclose(J @ d, Jo @ d, rtol=1e-13, atol=1e-9)
+
+
+def test_small_context_does_not_shrink_kernel_limits_of_a_larger_one():
+    """Kernel shared-memory limits are process-wide: a context of small
+    subdomains created after a larger one must not break the larger one's
+    launches (regression: cudaErrorInvalidValue from k_residual)."""
+    from paper_2411_00546_b200.schwarz import _sweep
+    cfg = CONFIGS["cfg2"]
+    spec = build_spec(cfg, with_matrix=False)
+    dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    big = build_local_systems(dec, spec)
+    tag, n, s1, s2, m, phi, nu, mu = UNIT_CASES[0]
+    small_spec = unit_spec(n, phi, nu, mu)
+    build_local_systems(decompose(small_spec.grid, s1, s2, m), small_spec)
+    x = big.from_host(np.zeros(cfg.unknowns))
+    _, inner = _sweep(big, x, big.factor_store(), ContinuationSchedule.fixed(1e-3),
+                      NewtonConfig(tol=1e-8))
+    assert max(inner) >= 1

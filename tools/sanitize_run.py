@@ -47,3 +47,52 @@ if "--all" in sys.argv:
     print("cfg1 newton-ras:", rep.converged, rep.outer_iters, rep.gmres_iters, flush=True)
     spec_t, pair = construct_test_problem(Grid(12), kappa=0.1, nu=1e-2, mu=1.0, k_tilde=2)
     print("manufactured test12:", float(np.abs(pair.y).max()), flush=True)
+
+if "--big" in sys.argv:   # oversized-block paths: config 4 (n = 172 corner), config 5 (ragged)
+    from paper_2411_00546_b200 import build_local_systems
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep, release_local_systems
+    for name, tol in (("cfg4", 1e-7), ("cfg5", 1e-8)):
+        c = CONFIGS[name]
+        sp_ = build_spec(c, with_matrix=False)
+        dc = decompose(sp_.grid, c.s1, c.s2, c.overlap)
+        eng = build_local_systems(dc, sp_)
+        xd = eng.from_host(np.zeros(c.unknowns))
+        fac = eng.factor_store()
+        sch = (ContinuationSchedule(c.eps0, c.gamma, c.eps_min) if name == "cfg4"
+               else ContinuationSchedule.fixed(c.eps_min))
+        fval, inner = _sweep(eng, xd, fac, sch, NewtonConfig(tol=tol, max_outer=200))
+        out = _jvp(eng, fac, eng.from_host(np.random.default_rng(1).standard_normal(c.unknowns)))
+        print(f"{name} sweep + JVP: inner max {max(inner)}, |fval| {fval.norm():.6e}, "
+              f"|jvp| {out.norm():.6e}", flush=True)
+        del out, fval, fac, xd, eng
+        release_local_systems(dc)
+
+# racecheck stand-in: the same solves repeated must be bitwise identical
+# (mbarrier rings, named barriers, grid barrier and tickets all feed
+# fixed-order reductions, so any race shows up as a changed bit)
+reps = int(os.environ.get("OCP_REPEAT", "0"))
+if reps:
+    ref = None
+    for r in range(reps):
+        x, rep = raspen_solve(np.zeros(cfg.unknowns), dec1, spec1, sched1,
+                              cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+                              krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000),
+                              inner_tol=1e-8)
+        key = (x.tobytes(), tuple(rep.gmres_iters), tuple(rep.residual_norms))
+        assert ref is None or key == ref, f"repeat {r} differs"
+        ref = key
+    print(f"{reps} repeated config-1 solves bitwise identical", flush=True)
+
+if os.environ.get("OCP_GUARD") == "1":
+    import ctypes
+    import gc
+    from paper_2411_00546_b200 import _native as nat
+    from paper_2411_00546_b200.schwarz import release_local_systems
+    release_local_systems(dec1)
+    gc.collect()
+    lib = nat.load()
+    bad, bufs = ctypes.c_longlong(), ctypes.c_longlong()
+    rc = lib.ocp_check_guards(ctypes.byref(bad), ctypes.byref(bufs))
+    print(f"guard zones: rc={rc} corrupted_bytes={bad.value} live_buffers={bufs.value} "
+          f"{nat.last_error(None) if bad.value else ''}", flush=True)
+    sys.exit(1 if rc or bad.value else 0)
