@@ -180,6 +180,30 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   if (!ok) *bad = 1;
 }
 
+#ifdef OCP_DFMA_ONLY
+// A/B build (tools/build_variant.py dfma -DOCP_DFMA_ONLY): the same tiles,
+// register layout and shared-memory operands, multiplied with DFMA instead of
+// DMMA - each lane accumulates its 16 (tile) / 16 (strip) outputs from one
+// A element per row and double2 B loads per k.  Justifies the DMMA choice
+// with a measurement (profiles/r2_dmma_vs_dfma.md).
+__device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
+                                           double c[4][2][2], int lane, double sgn) {
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const double2 b0 = *reinterpret_cast<const double2*>(B + k * ldb + 2 * t4);
+    const double2 b1 = *reinterpret_cast<const double2*>(B + k * ldb + 8 + 2 * t4);
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      const double am = sgn * A[(8 * mi + g) * lda + k];
+      c[mi][0][0] = fma(am, b0.x, c[mi][0][0]);
+      c[mi][0][1] = fma(am, b0.y, c[mi][0][1]);
+      c[mi][1][0] = fma(am, b1.x, c[mi][1][0]);
+      c[mi][1][1] = fma(am, b1.y, c[mi][1][1]);
+    }
+  }
+}
+#else
 // one 32x16 DMMA tile: C (+)= sgn * A[32 x 32] * B[32 x 16]
 //   A element (m, k) at A + m*lda + k ; B element (k, n) at B + k*ldb + n
 __device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
@@ -197,6 +221,7 @@ __device__ __forceinline__ void tile_32x16(const double* A, int lda, const doubl
     }
   }
 }
+#endif
 
 // C tile (32 x 16) at base (row stride lds) -> registers / back
 __device__ __forceinline__ void load_c(const double* base, int lds, double c[4][2][2], int lane) {
@@ -224,6 +249,24 @@ __device__ __forceinline__ void store_c(double* base, int lds, const double c[4]
 __device__ __forceinline__ void strip_16x32(double* A, const double* P, int lds, int lane) {
   const int g = lane >> 2, t4 = lane & 3;
   double c[2][4][2] = {};
+#ifdef OCP_DFMA_ONLY
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    double2 b[4];
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = *reinterpret_cast<const double2*>(P + k * lds + 8 * ni + 2 * t4);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const double am = -A[(8 * mi + g) * lds + k];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        c[mi][ni][0] = fma(am, b[ni].x, c[mi][ni][0]);
+        c[mi][ni][1] = fma(am, b[ni].y, c[mi][ni][1]);
+      }
+    }
+  }
+  __syncwarp();   // every lane has read its A rows before they are overwritten
+#else
 #pragma unroll
   for (int kk = 0; kk < 32; kk += 4) {
     double b[4];
@@ -236,6 +279,7 @@ __device__ __forceinline__ void strip_16x32(double* A, const double* P, int lds,
       for (int ni = 0; ni < 4; ++ni) dmma(c[mi][ni][0], c[mi][ni][1], am, b[ni]);
     }
   }
+#endif
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
