@@ -526,7 +526,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->fac_len = fac;
   ctx->ref_len = ref;
   ctx->maxWS = ctx->maxW + NBF;
-  if (ctx->maxW > MAX_W) {
+  if (ctx->fmt == 0 && ctx->maxW > MAX_W) {   // the band format's compiled window
     int code = fail(nullptr, OCP_ERR_UNSUPPORTED,
                     "local half-bandwidth %d exceeds the compiled limit %d", ctx->maxW, MAX_W);
     delete ctx;
@@ -642,8 +642,15 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   const int bf_per_sm = ctx->bf_narrow ? narrow_factor_ctas_per_sm() : 1;
   const int bf_max_npb = ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB;
   ctx->bf_grid = std::max(1, std::min(I, bf_per_sm * ctx->num_sms));
+  if (ctx->fmt == 1 && ctx->maxNPS > block_solve_max_nps()) {
+    fail(ctx, OCP_ERR_UNSUPPORTED, "local short side %d exceeds the block solve's limit %d",
+         ctx->maxNPS / 2, block_solve_max_nps() / 2);
+    return cleanup_fail(OCP_ERR_UNSUPPORTED);
+  }
   if (ctx->fmt == 1 && ctx->maxNPB > bf_max_npb) {
-    ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
+    // rows beyond the shared block, then (short side > 112) the line's
+    // Jacobian diagonals (k_block_factor)
+    ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4) + 2LL * ctx->maxNPB;
     CKC(gmalloc(&ctx->bscratch, ctx->bf_grid * ctx->bs_stride * sizeof(double)));
   }
   CKC(gmalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
@@ -665,21 +672,25 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   {
     int optin = 0;
     CKC(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    cudaFuncAttributes fa;
-    CKC(cudaFuncGetAttributes(&fa, k_band_factor));
-    if (factor_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
-      fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
-      return cleanup_fail(OCP_ERR_UNSUPPORTED);
+    if (ctx->fmt == 0) {   // band format (OCP_FACTOR_FORMAT=band)
+      cudaFuncAttributes fa;
+      CKC(cudaFuncGetAttributes(&fa, k_band_factor));
+      if (factor_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
+        fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
+        return cleanup_fail(OCP_ERR_UNSUPPORTED);
+      }
+      CKC(raise_smem_limit((const void*)k_band_factor, factor_smem_bytes(ctx->maxW)));
+      const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
+      if (solve_smem > optin) {
+        fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");
+        return cleanup_fail(OCP_ERR_UNSUPPORTED);
+      }
+      CKC(set_band_solve_smem(solve_smem));
     }
-    CKC(raise_smem_limit((const void*)k_band_factor, factor_smem_bytes(ctx->maxW)));
-    const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
-    if (solve_smem > optin) {
-      fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");
-      return cleanup_fail(OCP_ERR_UNSUPPORTED);
-    }
-    CKC(set_band_solve_smem(solve_smem));
     if (ctx->fmt == 1) {
-      const int fb = block_factor_smem_bytes(ctx->maxNPB), sb = (int)block_solve_smem_bytes(ctx->maxNPS);
+      // (lines wider than 224 unknowns use k_block_solve_wide, which sets its own limit)
+      const int fb = block_factor_smem_bytes(ctx->maxNPB),
+                sb = (int)block_solve_smem_bytes(std::min(ctx->maxNPS, 224));
       if (fb + 1024 > optin || sb + 1024 > optin) {
         fail(ctx, OCP_ERR_UNSUPPORTED, "block factor needs more shared memory than the device offers");
         return cleanup_fail(OCP_ERR_UNSUPPORTED);

@@ -73,6 +73,7 @@ void read_subt(long long* out, int n) {
 #define BPH_START() (void)0
 #define BPH_MARK(k) (void)0
 #endif
+constexpr int BF_JL_POINTS = 112;   // points per line whose diagonals fit the shared JL slot
 constexpr int BS_STAGES = 4;     // TMA ring depth of the solve
 #ifndef OCP_BS_PF_EARLY
 #define OCP_BS_PF_EARLY 0
@@ -317,7 +318,11 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
   // the Jacobian diagonals of the next line are loaded one line ahead
   // (registers) and staged in shared memory (JL) at the start of its E phase
   const int nq = 4 * s.nc;
-  double jn0 = tid < nq ? JD[tid] : 0.0, jn1 = tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
+  // lines of up to 2 BF_THREADS diagonal entries are prefetched in registers;
+  // wider ones (short side > 192) are copied at the start of their E phase
+  const bool jreg = nq <= 2 * BF_THREADS;
+  double jn0 = jreg && tid < nq ? JD[tid] : 0.0;
+  double jn1 = jreg && tid + BF_THREADS < nq ? JD[tid + BF_THREADS] : 0.0;
   // -W of a line goes to the factor store by TMA bulk stores (issued by warp
   // 0): the copies run on the TMA engine, so no global store traffic sits in
   // the load/store queues of the compute phases.  The shared block is
@@ -345,12 +350,16 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     __syncthreads();
   };
   for (int a = 0; a < nr; ++a) {
-    if (tid < nq) JL[tid] = jn0;
-    if (tid + BF_THREADS < nq) JL[tid + BF_THREADS] = jn1;
-    if (a + 1 < nr) {
-      const double* nx = JD + (long long)(a + 1) * nq;
-      jn0 = tid < nq ? nx[tid] : 0.0;
-      jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
+    if (jreg) {
+      if (tid < nq) JL[tid] = jn0;
+      if (tid + BF_THREADS < nq) JL[tid + BF_THREADS] = jn1;
+      if (a + 1 < nr) {
+        const double* nx = JD + (long long)(a + 1) * nq;
+        jn0 = tid < nq ? nx[tid] : 0.0;
+        jn1 = tid + BF_THREADS < nq ? nx[tid + BF_THREADS] : 0.0;
+      }
+    } else {
+      for (int t = tid; t < nq; t += BF_THREADS) JL[t] = JD[(long long)a * nq + t];
     }
     __syncthreads();   // JL complete: both warp groups read all of it in E2
     BPH_MARK(6);
@@ -368,49 +377,51 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     const bool grpA = warp < LAW;
     const int e_lo = grpA ? 0 : 32, e_hi = grpA ? 32 : NPB;
     const int e_w = grpA ? warp : warp - LAW, e_nw = grpA ? LAW : NW - LAW;
-    for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw) {
-      double2 v[2][4];
+    // (rows wider than 256 columns are processed in chunks of 256)
+    for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw)
+      for (int cb = 0; cb < NPB; cb += 256) {
+        double2 v[2][4];
 #pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 2 * lane + 64 * u;
-          v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(R.row(i0 + r) + j)
-                                       : make_double2(0.0, 0.0);
-        }
-      if (a > 0)
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int i = i0 + r, m16 = 16 * (i >> 4) + 16;
-          if (i >= NPS) continue;
-          double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, NPS / 16) +
-                                                    (long long)(i & 15) * (m16 + 2));
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int j = 2 * lane + 64 * u;
-            if (j < m16) __stcs(col + (j >> 1), v[r][u]);
+            const int j = cb + 2 * lane + 64 * u;
+            v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(R.row(i0 + r) + j)
+                                         : make_double2(0.0, 0.0);
           }
-        }
+        if (a > 0)
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int i = i0 + r;
-        double* rw = R.row(i);
+          for (int r = 0; r < 2; ++r) {
+            const int i = i0 + r, m16 = 16 * (i >> 4) + 16;
+            if (i >= NPS) continue;
+            double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, NPS / 16) +
+                                                      (long long)(i & 15) * (m16 + 2));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = 2 * lane + 64 * u;
-          if (j >= NPB) continue;
-          double2 w;
-          if (i < n && j < n) {
-            w.x = off2 * v[1 - r][u].y;
-            w.y = off2 * v[1 - r][u].x;
-          } else {
-            w.x = i == j ? 1.0 : 0.0;
-            w.y = i == j + 1 ? 1.0 : 0.0;
+            for (int u = 0; u < 4; ++u) {
+              const int j = cb + 2 * lane + 64 * u;
+              if (j < m16) __stcs(col + (j >> 1), v[r][u]);
+            }
           }
-          *reinterpret_cast<double2*>(rw + j) = w;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = i0 + r;
+          double* rw = R.row(i);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = cb + 2 * lane + 64 * u;
+            if (j >= NPB) continue;
+            double2 w;
+            if (i < n && j < n) {
+              w.x = off2 * v[1 - r][u].y;
+              w.y = off2 * v[1 - r][u].x;
+            } else {
+              w.x = i == j ? 1.0 : 0.0;
+              w.y = i == j + 1 ? 1.0 : 0.0;
+            }
+            *reinterpret_cast<double2*>(rw + j) = w;
+          }
         }
       }
-    }
     if (grpA) asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
     else asm volatile("bar.sync 3, %0;" ::"n"(BF_THREADS - 32 * LAW) : "memory");
     BPH_MARK(7);
@@ -592,6 +603,9 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     double* W0 = sm + SMEM_S;
     double* W1 = W0 + 32 * WLD;
     double* JL = W1 + 32 * WLD;
+    // lines wider than the shared JL slot (short side > BF_JL_POINTS) keep
+    // their diagonals after the scratch rows of this CTA
+    if (s.nc > BF_JL_POINTS) JL = gscratch + (long long)blockIdx.x * gs_stride + (long long)s.pad_ * lds;
     if (s.pad_ <= BF_SMEM_MAX_NPB) {
       factor_one<false>(s, JD, P.off, Rows<false>{sm, nullptr, s.pad_, lds}, fac, &bad, W0, W1, JL);
     } else {
@@ -618,8 +632,8 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
 int block_factor_threads() { return BF_THREADS; }
 
 int block_factor_smem_bytes(int max_npb) {
-  (void)max_npb;   // fixed layout: [S: 160 x 164][W0, W1: 32 x 33]
-  return (int)sizeof(double) * (BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4) + 2 * 32 * WLD + 4 * 112);
+  (void)max_npb;   // fixed layout: [S: 160 x 164][W0, W1: 32 x 33][JL: 4 x 112]
+  return (int)sizeof(double) * (BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4) + 2 * 32 * WLD + 4 * BF_JL_POINTS);
 }
 
 // ---------------------------------------------------------------------------
@@ -834,6 +848,189 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_block_solve_wide: the same solve for lines wider than the fast kernel's
+// limit (NPS > 224, i.e. a short side above 112 points: coarse
+// decompositions and the monolithic direct solve of newton[-eps]).
+// Warp w < NWC owns tile rows w, w + NWC, ... (TR of them, NWC <= 31);
+// the producer streams each tile column in units of G of its 16 columns
+// (G * (16c + 18) doubles <= WIDE_SBS), so any width fits the ring.  Row
+// and column parts are those of k_block_solve; tile columns are visited in
+// order 0 .. cpb-1 (two accumulators per row).
+// ---------------------------------------------------------------------------
+constexpr int WIDE_SBS = 4096;   // doubles per ring stage (32 KB)
+
+__host__ __device__ inline int wide_group(int cpb) {   // columns per unit
+  int g = 16;
+  while (g > 1 && (long long)g * (16 * (cpb - 1) + 18) > WIDE_SBS) g >>= 1;
+  return g;
+}
+
+template <int MODE, int TR>
+__global__ void __launch_bounds__(1024, 1)
+k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
+                   const double* in_pool, double scale, double* out_pool, double off, int max_nps,
+                   const double* dglob, double* oglob, int gn) {
+  extern __shared__ __align__(16) double sm[];
+  const SubInfo s = subs[list[blockIdx.x]];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NPS = s.NPS, n = 2 * s.nc, nr = s.nr, cpb = NPS / 16;
+  const int NWC = (cpb + TR - 1) / TR;                // consumer warps of this subdomain
+  const int G = wide_group(cpb), upc = 16 / G, nunits = cpb * upc;
+  double* stage = sm;                                 // [BS_STAGES][WIDE_SBS]
+  double* vp = sm + BS_STAGES * WIDE_SBS;             // [2][max_nps]
+  __shared__ __align__(8) uint64_t full[BS_STAGES], empty[BS_STAGES];
+  const double* fac = fac_pool + s.fac;
+  const double* in = in_pool + s.loc;
+  double* out = out_pool + s.loc;
+  const long long lsz = block_line_doubles(NPS);
+  int a_stop = 0;
+  if (MODE >= 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+  const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;
+  const int nlines = nr + nback;
+  if (tid == 0) {
+    for (int i = 0; i < BS_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NWC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = tid; t < NPS; t += blockDim.x)
+    vp[t ^ 1] = t < n ? (MODE == 2 ? jvp_rhs(s, dglob, gn, off, 0, t)
+                         : MODE == 3 ? ras_rhs(s, dglob, gn, 0, t) : scale * in[t]) : 0.0;
+  __syncthreads();
+  auto line_of = [&](int b) { return b < nr ? b : nr - 2 - (b - nr); };
+  if (warp == (int)(blockDim.x >> 5) - 1) {
+    if (lane == 0) {
+      const long long total = (long long)nlines * nunits;
+      for (long long t = 0; t < total; ++t) {
+        const int st = (int)(t % BS_STAGES);
+        if (t >= BS_STAGES) mbar_wait(&empty[st], (uint32_t)(((t / BS_STAGES) - 1) & 1));
+        const int blk = (int)(t / nunits), u = (int)(t % nunits);
+        const int c = u / upc, q0 = (u % upc) * G, ld2 = 16 * c + 18;
+        const double* src = fac + line_of(blk) * lsz + block_col_off(c, cpb) + (long long)q0 * ld2;
+        const uint32_t bytes = (uint32_t)(8 * G * ld2);
+        mbar_expect_tx(&full[st], bytes);
+        bulk_g2s(stage + st * WIDE_SBS, src, bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  if (warp >= NWC) return;
+  const int jj = lane & 15, h = lane >> 4;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int blk = 0; blk < nlines; ++blk) {
+    const bool fwd = blk < nr;
+    const int a = line_of(blk);
+    const double* v = vp + (blk & 1) * max_nps;
+    double* vnext = vp + ((blk + 1) & 1) * max_nps;
+    double acc[TR][2];
+#pragma unroll
+    for (int r = 0; r < TR; ++r) acc[r][0] = acc[r][1] = 0.0;
+    for (int u = 0; u < nunits; ++u) {
+      const int c = u / upc, q0 = (u % upc) * G, ld2 = 16 * c + 18;
+      mbar_wait(&full[st], ph);
+      const double* cb = stage + st * WIDE_SBS;   // columns q0 .. q0+G-1 of tile column c
+#pragma unroll
+      for (int r = 0; r < TR; ++r) {
+        const int ti = warp + NWC * r;
+        if (ti >= cpb) continue;
+        const int i = 16 * ti + jj;
+        if (c >= ti) {   // row part: columns 8h .. 8h+7 of tile (ti, c) inside this unit
+          const int k0 = max(8 * h, q0), k1 = min(8 * h + 8, q0 + G);
+          for (int q = k0; q < k1; ++q) acc[r][q & 1] = fma(cb[(q - q0) * ld2 + i], v[16 * c + q], acc[r][q & 1]);
+        }
+        if (c == ti && jj >= q0 && jj < q0 + G) {   // column part: stored column i above the diagonal tile
+          const double* cj = cb + (jj - q0) * ld2 + 2 * h;
+          const double* vr = v + 2 * h;
+          for (int rr = 0; rr < 16 * c; rr += 4) {
+            const double2 x = *reinterpret_cast<const double2*>(cj + rr);
+            const double2 y = *reinterpret_cast<const double2*>(vr + rr);
+            acc[r][0] = fma(x.x, y.x, acc[r][0]);
+            acc[r][1] = fma(x.y, y.y, acc[r][1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == BS_STAGES) { st = 0; ph ^= 1; }
+    }
+#pragma unroll
+    for (int r = 0; r < TR; ++r) {
+      const int ti = warp + NWC * r;
+      if (ti >= cpb) continue;
+      const int i = 16 * ti + jj;
+      double y = -(acc[r][0] + acc[r][1]);        // the store holds -W
+      y += __shfl_xor_sync(0xffffffffu, y, 16);
+      if (h == 0) {
+        double nxt = 0.0;
+        if (i < n) {
+          if (fwd) {
+            if (a + 1 < nr)
+              nxt = MODE == 2 ? jvp_rhs(s, dglob, gn, off, a + 1, i)
+                    : MODE == 3 ? ras_rhs(s, dglob, gn, a + 1, i) : in[(long long)(a + 1) * n + i];
+          } else {
+            nxt = out[(long long)a * n + i];
+          }
+        }
+        double x = 0.0;
+        if (fwd) {
+          const double w = i < n ? y : 0.0;
+          if (i < n && (MODE < 2 || a + 1 < nr)) out[(long long)a * n + i] = w;
+          vnext[i ^ 1] = (a + 1 < nr) ? (i < n ? fma(-off, w, scale * nxt) : 0.0) : w;
+          x = w;
+        } else {
+          x = i < n ? fma(-off, y, nxt) : 0.0;
+          if (MODE < 2 && i < n) out[(long long)a * n + i] = x;
+          vnext[i ^ 1] = x;
+        }
+        if (MODE >= 2 && (!fwd || a + 1 == nr) && i < n) {
+          int gi, gj;
+          local_to_global(s, a, i >> 1, gi, gj);
+          if (gi >= s.or0 && gi < s.or1 && gj >= s.oc0 && gj < s.oc1) {
+            const long long g = (long long)(i & 1) * gn * gn + (long long)gi * gn + gj;
+            oglob[g] = MODE == 2 ? -add(dglob[g], x) : x;
+          }
+        }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * NWC) : "memory");
+  }
+}
+
+size_t block_solve_wide_smem_bytes(int max_nps) {
+  return sizeof(double) * ((size_t)BS_STAGES * WIDE_SBS + 2 * (size_t)max_nps);
+}
+
+template <int MODE>
+static cudaError_t launch_wide_mode(int grid, cudaStream_t st, const SubInfo* subs, const int* list,
+                                    const double* fac, const double* in, double scale,
+                                    double* out_pool, double off, int max_nps, const double* dglob,
+                                    double* oglob, int gn) {
+  const int cpb = max_nps / 16;
+  const size_t smem = block_solve_wide_smem_bytes(max_nps);
+  int tr = 1;
+  while ((cpb + tr - 1) / tr > 31) tr *= 2;
+  const int nt = 32 * ((cpb + tr - 1) / tr + 1);
+#define OCP_WIDE(TRV)                                                                           \
+  do {                                                                                          \
+    cudaError_t e = raise_smem_limit((const void*)k_block_solve_wide<MODE, TRV>, (int)smem);    \
+    if (e != cudaSuccess) return e;                                                             \
+    k_block_solve_wide<MODE, TRV><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, \
+                                                          off, max_nps, dglob, oglob, gn);      \
+  } while (0)
+  if (tr == 1) OCP_WIDE(1);
+  else if (tr == 2) OCP_WIDE(2);
+  else if (tr == 4) OCP_WIDE(4);
+  else if (tr == 8) OCP_WIDE(8);
+  else return cudaErrorInvalidConfiguration;   // NPS > 3968: short side above 1984 points
+#undef OCP_WIDE
+  return cudaGetLastError();
+}
+
+int block_solve_max_nps() { return 16 * 31 * 8; }
+
 size_t block_solve_smem_bytes(int max_npb) {
   return sizeof(double) * ((size_t)BS_STAGES * bs_stage_doubles(max_npb) + 2 * (size_t)max_npb);
 }
@@ -844,7 +1041,12 @@ cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInf
                                double* oglob, int gn) {
   const size_t smem = block_solve_smem_bytes(max_npb);
   const int nt = bs_threads(max_npb);
-  if (nt > BS_MAX_THREADS) return cudaErrorInvalidConfiguration;
+  if (nt > BS_MAX_THREADS) {   // short side above 112 points
+    if (mode == 0) return launch_wide_mode<0>(grid, st, subs, list, fac, in, scale, out_pool, off, max_npb, dglob, oglob, gn);
+    if (mode == 1) return launch_wide_mode<1>(grid, st, subs, list, fac, in, scale, out_pool, off, max_npb, dglob, oglob, gn);
+    if (mode == 2) return launch_wide_mode<2>(grid, st, subs, list, fac, in, scale, out_pool, off, max_npb, dglob, oglob, gn);
+    return launch_wide_mode<3>(grid, st, subs, list, fac, in, scale, out_pool, off, max_npb, dglob, oglob, gn);
+  }
   if (mode == 0)
     k_block_solve<0><<<grid, nt, smem, st>>>(subs, list, fac, in, scale, out_pool, off, max_npb,
                                              dglob, oglob, gn);

@@ -98,6 +98,7 @@ __global__ void k_block_factor(const SubInfo* subs, const int* list, int cnt, Ph
 int block_factor_smem_bytes(int max_npb);
 int block_factor_threads();
 size_t block_solve_smem_bytes(int max_npb);
+int block_solve_max_nps();
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
                                const int* list, const double* fac, const double* in, double scale,
                                double* out_pool, double off, int max_npb,

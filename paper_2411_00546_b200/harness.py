@@ -11,7 +11,8 @@ repr, fields by ``%.17g``).  Every method runs on the device:
 * ``newton-ras`` / ``newton-ras-eps`` -> ``linear_ras.newton_ras_solve``
 * ``newton`` / ``newton-eps``      -> monolithic Newton on the global residual;
   ``linear_solver`` auto/direct: one banded LU of the whole Jacobian
-  (single-subdomain engine, n <= 112), gmres: unpreconditioned device GMRES.
+  (single-subdomain engine, block factor of the whole grid), gmres: unpreconditioned
+  device GMRES.
 
 The manufactured problem of ``build_problem`` is set up on the device
 (``problem_setup.construct_test_problem``).

@@ -81,7 +81,8 @@ class GlobalJacobian:
     def direct_solve(self, rhs):
         """Sparse direct solve of J d = rhs (splu, `newton.py:125-129`): the
         batched banded LU on a single-subdomain engine, i.e. one LU of the
-        whole Jacobian (half-bandwidth 2n: grids up to n = 112)."""
+        whole Jacobian (block-tridiagonal factor of 2n-unknown lines; any n up to
+        1984, lines wider than 224 unknowns on the wide kernels)."""
         if self.engine.num_subdomains != 1:
             raise ValueError("direct solves need the single-subdomain (1x1) engine")
         if self._lu is None:

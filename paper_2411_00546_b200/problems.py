@@ -78,6 +78,17 @@ CONFIGS = {
 }
 
 
+# Not BASELINE rows: coarse decompositions whose local short side exceeds the
+# fast kernels' 112 points (the paper's 2x2 at N = 450 has 227), used by the
+# wide-line parity tests against reference fixtures (tests/golden/wide.npz).
+EXTRA_CONFIGS = {
+    "wide2x2": BaselineConfig("wide2x2", 300, "cubic", 1e-3, 1e-2, 2, 2, 8,
+                              1.0, 0.1, 1e-6, "zero", "bumps", bumps=8),
+    "mono150": BaselineConfig("mono150", 150, "cubic", 1e-3, 1e-2, 1, 1, 0,
+                              1.0, 0.1, 1e-6, "zero", "bumps", bumps=8),
+}
+
+
 def _bumps(grid, rng, k, centers, widths, amps):
     x1, x2 = grid.points()
     c = rng.uniform(centers[0], centers[1], size=(k, 2))

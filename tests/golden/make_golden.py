@@ -406,6 +406,67 @@ def run_ras_solve(name, out_path):
           f"wall={wall:.1f}s")
 
 
+def run_wide(out_path):
+    """Decompositions beyond the fast kernels' 112-point short side.
+
+    * ``wide2x2``: raspen_solve on a 300^2 grid, 2x2 subdomains, overlap 8
+      (local short side 158; harness settings, inner tol 1e-8);
+    * ``mono150``: monolithic newton-eps with the direct (SuperLU) direction
+      on a 150^2 grid (`harness/experiments.py:86-91`), i.e. one banded
+      solve of the whole 2 x 22500-unknown Jacobian per Newton step.
+    """
+    from ocp.newton import newton_continuation
+    from ocp.system import residual, jacobian
+    from paper_2411_00546_b200.problems import EXTRA_CONFIGS
+
+    data = {}
+    cfg = EXTRA_CONFIGS["wide2x2"]
+    spec = ref_spec(cfg)
+    dec = ref_schwarz.decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)
+    sched = ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)
+    t0 = time.perf_counter()
+    with PerSubRecorder() as rec:
+        x, rep = ref_schwarz.raspen_solve(
+            np.zeros(2 * spec.grid.size), dec, spec, sched,
+            cfg=NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1),
+            krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000), inner_tol=1e-8, threads=4)
+    print(f"wide2x2: conv={rep.converged} outer={rep.outer_iters} inner={rep.inner_iters} "
+          f"gmres={rep.gmres_iters} wall={time.perf_counter() - t0:.1f}s", flush=True)
+    _store_solve(data, "wide2x2", cfg, spec, x, rep)
+    data["wide2x2_per_sub"] = np.array(rec.per_eval(len(dec)), dtype=np.int64)
+
+    cfg = EXTRA_CONFIGS["mono150"]
+    spec = ref_spec(cfg)
+    sched = ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)
+    t0 = time.perf_counter()
+    x, rep = newton_continuation(np.zeros(2 * spec.grid.size),
+                                 lambda x, eps: residual(x, spec, eps, check=False),
+                                 lambda x, eps: jacobian(x, spec, eps), sched,
+                                 NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1,
+                                              linear_solver="direct"))
+    print(f"mono150: conv={rep.converged} outer={rep.outer_iters} alphas={rep.alphas} "
+          f"wall={time.perf_counter() - t0:.1f}s", flush=True)
+    _store_solve(data, "mono150", cfg, spec, x, rep)
+    np.savez_compressed(out_path, **data)
+
+
+def _store_solve(data, tag, cfg, spec, x, rep):
+    n2 = spec.grid.size
+    y, p = x[:n2], x[n2:]
+    u = recover_control(p, spec, cfg.eps_min)
+    data[f"{tag}_converged"] = rep.converged
+    data[f"{tag}_outer"] = rep.outer_iters
+    data[f"{tag}_inner"] = np.array(rep.inner_iters)
+    data[f"{tag}_gmres"] = np.array([-1 if k is None else k for k in rep.gmres_iters])
+    data[f"{tag}_alphas"] = np.array(rep.alphas)
+    data[f"{tag}_norms"] = np.array(rep.residual_norms)
+    for key, vec in (("y", y), ("p", p), ("u", u)):
+        for k, v in digest(vec).items():
+            data[f"{tag}_{key}_{k}"] = v
+    for k, v in support_bits(p, cfg.mu, cfg.eps_min).items():
+        data[f"{tag}_{k}"] = v
+
+
 HARNESS_CASES = [
     ("newton_eps", dict(method="newton-eps")),
     ("newton", dict(method="newton", eps0=1e-3)),
@@ -458,6 +519,8 @@ def main():
         run_units(args.out or os.path.join(HERE, "units.npz"))
     elif args.what == "harness":
         run_harness(args.out or os.path.join(HERE, "harness.npz"))
+    elif args.what == "wide":
+        run_wide(args.out or os.path.join(HERE, "wide.npz"))
     elif args.what == "variants":
         run_variants(args.out or os.path.join(HERE, "variants.npz"))
     elif args.what == "ras_units":
