@@ -57,6 +57,7 @@ struct ocp_ctx {
   double *V = nullptr, *R = nullptr, *D = nullptr, *B = nullptr, *JD = nullptr;
   int *d_list_all = nullptr, *d_list = nullptr, *d_status = nullptr, *d_flags = nullptr;
   double *d_alpha = nullptr, *d_norm2 = nullptr, *d_rpart = nullptr;
+  unsigned long long* d_rbad = nullptr;   // per (subdomain, residual CTA) first bad phi'/phi
   unsigned int* d_rcount = nullptr;
   int res_chunks = 1;
   int res_smem = 0;           // dynamic shared memory of k_residual
@@ -316,17 +317,19 @@ double band_lu_flops(long long N, long long w) {
 
 // local residual (+ per-subdomain squared norms) of `cnt` listed subdomains
 int launch_residual(ocp_ctx* ctx, const int* d_list, int cnt, const double* x, const double* V,
-                    const double* D, const double* alpha, double eps, double* R) {
+                    const double* D, const double* alpha, double eps, double* R, bool jd = false) {
   if (cnt == 0) return OCP_OK;
   // full-set residual evaluations are timed for the stencil roofline
-  // (48 B per local point: read y,p,f,y_d, write r1,r2 - SURVEY.md 8d)
-  Timer t(cnt == ctx->I && !D ? ctx : nullptr, CLS_RESID, 0, ctx->resid_bytes_all);
+  // (48 B per local point: read y,p,f,y_d, write r1,r2 - SURVEY.md 8d; with
+  // the fused Jacobian diagonals 80 B: + the (dg, b12, b21, 0) write)
+  Timer t(cnt == ctx->I && !D ? ctx : nullptr, CLS_RESID, 0,
+          ctx->resid_bytes_all * (jd ? 80.0 / 48.0 : 1.0));
   const dim3 grid(cnt, ctx->res_chunks);
   // every list is an ascending subset of the subdomains, so a full-count
   // list is the identity: the kernel then skips the list indirection
   k_residual<<<grid, RES_THREADS, ctx->res_smem, ctx->stream>>>(
       ctx->d_subs, cnt == ctx->I ? nullptr : d_list, ctx->P, x, V, D, alpha, ctx->d_f, ctx->d_yd, eps, R, ctx->d_norm2,
-      ctx->d_rpart, ctx->d_rcount);
+      ctx->d_rpart, ctx->d_rcount, jd ? ctx->JD : nullptr, ctx->d_rbad, ctx->d_bad);
   CKL();
   return OCP_OK;
 }
@@ -467,6 +470,8 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->P.off = -1.0 / h2;
   ctx->P.nu = nu;
   ctx->P.mu = mu;
+  ctx->P.rnu = 1.0 / nu;   // correctly rounded on the host (dvd_const)
+  ctx->P.rmu = 1.0 / mu;
   ctx->P.kappa = kappa;
   ctx->P.kappa2 = kappa * kappa;
   long long loc = 0, fac = 0, ref = 0;
@@ -592,6 +597,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     CKC(raise_smem_limit((const void*)k_residual, ctx->res_smem));
   }
   CKC(gmalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
+  CKC(gmalloc(&ctx->d_rbad, (size_t)I * ctx->res_chunks * sizeof(unsigned long long)));
   CKC(gmalloc(&ctx->d_rcount, I * sizeof(unsigned int)));
   CKC(cudaMemset(ctx->d_rcount, 0, I * sizeof(unsigned int)));
   CKC(gmalloc(&ctx->d_bad, I * sizeof(long long)));
@@ -718,7 +724,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
@@ -834,7 +840,9 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
   k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, x, ctx->V);
   CKL();
   double eps = eps0;
-  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->V, nullptr, nullptr, eps, ctx->R)) return rc;
+  // the first residual also produces the Jacobian diagonals at eps0
+  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->V, nullptr, nullptr, eps, ctx->R, true))
+    return rc;
   CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int i = 0; i < I; ++i) {
@@ -870,8 +878,8 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
     if (act.empty()) break;
     const int cnt = (int)act.size();
     if (int rc = upload_list(ctx, act)) return rc;
-    k_jacdiag<<<cnt, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->P, ctx->V, eps, ctx->JD, ctx->d_bad);
-    CKL();
+    // the Jacobian diagonals at (V, eps) came with the residual that accepted
+    // the last step (or the first residual): every active subdomain was in it
     if (int rc = launch_factor(ctx, ctx->d_list, act, fac)) return rc;
     if (int rc = launch_solve(ctx, ctx->d_list, act, fac, ctx->R, -1.0, ctx->D, CLS_INNER_SOLVE)) return rc;
     CK(cudaMemcpyAsync(ctx->h_bad, ctx->d_bad, I * sizeof(long long), cudaMemcpyDeviceToHost, st));
@@ -928,7 +936,8 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
       const int na = (int)acc.size();
       k_update<<<na, 256, 0, st>>>(ctx->d_subs, ctx->d_list, ctx->V, ctx->D, ctx->d_alpha);
       CKL();
-      if (int rc = launch_residual(ctx, ctx->d_list, na, x, ctx->V, nullptr, nullptr, eps_next, ctx->R))
+      if (int rc = launch_residual(ctx, ctx->d_list, na, x, ctx->V, nullptr, nullptr, eps_next, ctx->R,
+                                   true))
         return rc;
       CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));

@@ -92,6 +92,11 @@ __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const dou
 // are read at the point's global index (coalesced for orient 0, per-lane
 // strided rows for orient 1) before the staging barrier; the residual is
 // stored at q (coalesced).
+// With JD != null (the residual of an accepted step, or the first one) the
+// Jacobian diagonals of the same values and eps are produced as well - what
+// k_jacdiag would compute next - sharing x = -p/mu, the two square roots of
+// P_eps and phi'(y); *badkey receives this CTA's first nonfinite phi'/phi''
+// (k_jacdiag's packed key).  Every value is bitwise k_jacdiag's.
 template <int OR>
 __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
                                                 const double* __restrict__ x,
@@ -99,7 +104,9 @@ __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
                                                 const double2* __restrict__ D, double al,
                                                 const double* __restrict__ f,
                                                 const double* __restrict__ yd, double eps,
-                                                double2* __restrict__ R, int base, double2* tv) {
+                                                double2* __restrict__ R, int base, double2* tv,
+                                                double2* __restrict__ JD,
+                                                unsigned long long& badkey) {
   constexpr int PPT = RQ / RES_THREADS;
   const int nr = s.nr, nc = s.nc, n = P.n, real = nr * nc;
   const long long Ntot = (long long)n * n;
@@ -185,11 +192,35 @@ __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
       }
     }
     const double ay = add(sly, sey), ap = add(slp, sep);
-    double r1, r2;
-    residual_rows(P, ay, ap, cv.x, cv.y, fv[u], ydv[u], eps, r1, r2);
+    const double y = cv.x, p = cv.y;
+    // residual_rows (system.py:118-132) with the smoothed projection's parts kept
+    const double xm = dvd_const(-p, P.mu, P.rmu), a1 = add(xm, 1.0), b1 = sub(xm, 1.0);
+    const double sa = __dsqrt_rn(add(mul(a1, a1), eps)), sb = __dsqrt_rn(add(mul(b1, b1), eps));
+    const double d1 = phi_d1(P, y);
+    const double ctrl = dvd_const(add(p, mul(P.mu, mul(0.5, sub(sa, sb)))), P.nu, P.rnu);
+    const double r1 = add(sub(add(ay, phi_value(P, y)), fv[u]), ctrl);
+    const double r2 = add(sub(add(ap, mul(d1, p)), y), ydv[u]);
     acc = fma(r1, r1, acc);
     acc = fma(r2, r2, acc);
     if (R) R[q] = make_double2(r1, r2);
+    if (JD) {   // jacobian_diagonals (system.py:135-144), k_jacdiag's operation order
+      const double d2 = phi_d2(P, y);
+      bool bad1 = !isfinite(d1), bad2 = !isfinite(d2);
+      if (P.phi_kind == 0 && P.kappa != 0.0 && mul(P.kappa, y) > 700.0) bad1 = bad2 = true;
+      if (P.phi_kind == 2 && y > 700.0) bad1 = bad2 = true;
+      if (bad1 || bad2) {
+        const int i = OR == 0 ? s.r0 + la[u] : s.r0 + lb[u];
+        const int j = OR == 0 ? s.c0 + lb[u] : s.c0 + la[u];
+        const unsigned long long ref = (unsigned long long)((i - s.r0) * (s.c1 - s.c0) + (j - s.c0));
+        const unsigned long long key = ((bad1 ? 0ull : 1ull) << 32) | ref;
+        badkey = key < badkey ? key : badkey;
+      }
+      const double dp = mul(0.5, sub(dvd(a1, sa), dvd(b1, sb)));
+      const double b12 = dvd_const(sub(1.0, dp), P.nu, P.rnu);
+      const double b21 = sub(mul(d2, p), 1.0);
+      JD[2 * q] = make_double2(add(P.diag, d1), b12);
+      JD[2 * q + 1] = make_double2(b21, 0.0);
+    }
   }
   return acc;
 }
@@ -201,9 +232,11 @@ __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const Su
                                                       const double* Dpool, const double* alpha,
                                                       const double* f, const double* yd, double eps,
                                                       double* Rpool, double* norm2, double* partials,
-                                                      unsigned int* counters) {
+                                                      unsigned int* counters, double* JDpool,
+                                                      unsigned long long* badparts, long long* bad) {
   extern __shared__ double2 tv[];
   __shared__ double red[32];
+  __shared__ unsigned long long bmin;
   __shared__ bool is_last;
   const int sid = list ? list[blockIdx.x] : blockIdx.x;   // null list: all subdomains
   const SubInfo s = subs[sid];
@@ -212,14 +245,19 @@ __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const Su
   double2* R = Rpool ? reinterpret_cast<double2*>(Rpool + s.loc) : nullptr;
   const double al = alpha ? alpha[sid] : 0.0;
   const int base = blockIdx.y * RQ;
+  double2* JD = JDpool ? reinterpret_cast<double2*>(JDpool + 2 * s.loc) : nullptr;
+  if (JD && threadIdx.x == 0) bmin = ~0ull;
   double acc = 0.0;
+  unsigned long long key = ~0ull;
   if (base < s.nr * s.nc) {
-    acc = s.orient == 0 ? residual_flat<0>(s, P, x, V, D, al, f, yd, eps, R, base, tv)
-                        : residual_flat<1>(s, P, x, V, D, al, f, yd, eps, R, base, tv);
+    acc = s.orient == 0 ? residual_flat<0>(s, P, x, V, D, al, f, yd, eps, R, base, tv, JD, key)
+                        : residual_flat<1>(s, P, x, V, D, al, f, yd, eps, R, base, tv, JD, key);
   }
+  if (JD && key != ~0ull) atomicMin(&bmin, key);   // (bmin set before the staging barrier)
   const double tot = block_sum<RES_THREADS>(acc, red);
   if (threadIdx.x == 0) {
     partials[(long long)sid * gridDim.y + blockIdx.y] = tot;
+    if (JD) badparts[(long long)sid * gridDim.y + blockIdx.y] = bmin;
     __threadfence();
     const unsigned int ticket = atomicAdd(&counters[sid], 1u);
     is_last = (ticket == gridDim.y - 1);
@@ -228,8 +266,16 @@ __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const Su
   if (is_last && threadIdx.x == 0) {
     __threadfence();
     double v = 0.0;
-    for (int y = 0; y < (int)gridDim.y; ++y) v += partials[(long long)sid * gridDim.y + y];
+    unsigned long long b = ~0ull;
+    for (int y = 0; y < (int)gridDim.y; ++y) {
+      v += partials[(long long)sid * gridDim.y + y];
+      if (JD) {
+        const unsigned long long by = badparts[(long long)sid * gridDim.y + y];
+        b = by < b ? by : b;
+      }
+    }
     norm2[sid] = v;
+    if (JD) bad[sid] = b == ~0ull ? -1ll : (long long)b;
     counters[sid] = 0u;
   }
 }

@@ -23,7 +23,8 @@ size_t residual_smem_bytes(int max_nc);
 __global__ void k_residual(const SubInfo* subs, const int* list, Phys P, const double* x,
                            const double* Vpool, const double* Dpool, const double* alpha,
                            const double* f, const double* yd, double eps, double* Rpool,
-                           double* norm2, double* partials, unsigned int* counters);
+                           double* norm2, double* partials, unsigned int* counters,
+                           double* JDpool, unsigned long long* badparts, long long* bad);
 __global__ void k_jacdiag(const SubInfo* subs, const int* list, Phys P, const double* Vpool,
                           double eps, double* JDpool, long long* bad);
 __global__ void k_update(const SubInfo* subs, const int* list, double* Vpool, const double* Dpool,
