@@ -233,7 +233,12 @@ def run_ours(args):
     dist.barrier()
     engine.sync()
     engine.mark(0)
+    if args.profile_window:   # ncu --profile-from-start off: capture the timed steps only
+        torch.cuda.cudart().cudaProfilerStart()
     reps = [step() for _ in range(args.steps)]
+    if args.profile_window:
+        engine.sync()
+        torch.cuda.cudart().cudaProfilerStop()
     engine.mark(1)
     engine.sync()
     dist.barrier()
@@ -588,6 +593,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stress", action="store_true", help="skip the config-5 stress timing")
+    ap.add_argument("--profile-window", action="store_true",
+                    help="cudaProfilerStart/Stop around the timed steps (ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
