@@ -124,7 +124,7 @@ int ocp_local_values(ocp_ctx* ctx, double* values_dev);
 /* Parity hooks for the kernels: local residual of every subdomain at local
  * values v (reference layout) with the exterior frozen at x
  * (_local_problem.local_residual, schwarz.py:181-186), and one Newton
- * direction -J(v)^{-1} F(v) by the batched banded LU (newton.py:127). */
+ * direction -J(v)^{-1} F(v) by the batched block-Thomas factor (newton.py:127). */
 int ocp_local_residual(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
                        double eps, double* r_ref_dev);
 int ocp_local_direction(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
@@ -181,7 +181,7 @@ int ocp_global_jacobian(ocp_ctx* ctx, const double* x_dev, double eps, double* j
 /* out = J d, the CSR row sums of jacobian(x) @ d  (system.py:155-160) */
 int ocp_global_jvp(ocp_ctx* ctx, const double* jd_dev, const double* d_dev, double* out_dev);
 /* ras_preconditioner build (schwarz.py:221-232): local pair Jacobians at
- * x[pair_idx] of every subdomain, batched banded LU into fac_dev (a factor
+ * x[pair_idx] of every subdomain, batched block factor into fac_dev (a factor
  * store as for ocp_raspen_residual).  OCP_ERR_LOCAL_SOLVE ("singular local
  * block") / OCP_ERR_NONFINITE with *failed_sub = subdomain. */
 int ocp_ras_factor(ocp_ctx* ctx, const double* x_dev, double eps, double* fac_dev,

@@ -12,7 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libocpgpu.so")
-SOURCES = ["ocp_abi.cu", "ocp_kernels.cu", "ocp_band.cu", "ocp_solve.cu", "ocp_krylov.cu", "ocp_global.cu", "ocp_block.cu", "ocp_block_narrow.cu"]
+SOURCES = ["ocp_abi.cu", "ocp_kernels.cu", "ocp_krylov.cu", "ocp_global.cu", "ocp_block.cu",
+           "ocp_block_narrow.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -52,7 +52,7 @@ struct ocp_ctx {
   std::vector<long long> sub_dofs;  // 2 R C
   SubInfo* d_subs = nullptr;
   long long pool_len = 0, fac_len = 0, ref_len = 0, dof_total = 0;
-  int maxW = 0, maxNP = 0, maxWS = 0;
+  int maxW = 0, maxNP = 0;
   double *d_f = nullptr, *d_yd = nullptr;
   double *V = nullptr, *R = nullptr, *D = nullptr, *B = nullptr, *JD = nullptr;
   int *d_list_all = nullptr, *d_list = nullptr, *d_status = nullptr, *d_flags = nullptr;
@@ -62,9 +62,6 @@ struct ocp_ctx {
   int res_chunks = 1;
   int res_smem = 0;           // dynamic shared memory of k_residual
   long long* d_bad = nullptr;
-  double* scratch = nullptr;
-  long long ws_stride = 0;
-  int fmt = 1;                 // factor format: 0 banded LU, 1 block tridiagonal (ocp_block.cu)
   int maxNPB = 0, maxNPS = 0;
   int* d_flist = nullptr;      // block format: factor list ordered by decreasing cost
   int* d_solve_order = nullptr;   // launch order of full-list block solves
@@ -73,7 +70,7 @@ struct ocp_ctx {
   long long bs_stride = 0;
   int bf_grid = 1;
   bool bf_narrow = false;     // narrow-line factor instance (ocp_block_narrow.cu)
-  int lu_grid = 1, num_sms = 148;
+  int num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
   unsigned long long* arn_bar = nullptr;   // split grid barrier of the Arnoldi kernel
@@ -347,7 +344,7 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   double flops = 0;
   for (int i : list) flops += ctx->sub_flops[i];
   Timer t(ctx, CLS_FACTOR, flops);
-  if (ctx->fmt == 1) {
+  {
     // persistent CTAs take subdomains in list order: largest work first
     // (global-memory Schur blocks, then nr * NPB^3), so the tail is short
     if (!ctx->d_flist) {   // list + the work counter of the persistent CTAs
@@ -378,21 +375,13 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     CKL();
     return OCP_OK;
   }
-  const int grid = std::min(cnt, ctx->lu_grid);
-  k_band_factor<<<grid, LU_THREADS, factor_smem_bytes(ctx->maxW), ctx->stream>>>(
-      ctx->d_subs, d_list, cnt, ctx->P, ctx->JD, fac, ctx->scratch, ctx->ws_stride, ctx->d_status);
-  CKL();
-  return OCP_OK;
 }
 
 cudaError_t any_solve(ocp_ctx* ctx, int mode, int cnt, const int* d_list, const double* fac,
                       const double* in, double scale, double* out) {
-  if (ctx->fmt == 1)
-    return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs,
-                              cnt == ctx->I ? ctx->d_solve_order : d_list, fac, in, scale, out,
-                              ctx->P.off, ctx->maxNPS);
-  return launch_band_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out,
-                           ctx->maxW);
+  return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs,
+                            cnt == ctx->I ? ctx->d_solve_order : d_list, fac, in, scale, out,
+                            ctx->P.off, ctx->maxNPS);
 }
 
 int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, const double* fac,
@@ -475,7 +464,6 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->P.kappa = kappa;
   ctx->P.kappa2 = kappa * kappa;
   long long loc = 0, fac = 0, ref = 0;
-  if (const char* e = getenv("OCP_FACTOR_FORMAT")) ctx->fmt = (std::string(e) == "band") ? 0 : 1;
   for (auto& r : rt) {
     for (auto& c : ct) {
       SubInfo s{};
@@ -506,12 +494,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       // the JVP needs x only on the ownership block: the backward sweep stops
       // at its first oriented line (MODE 1 of both solve kernels)
       const int a_own = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
-      if (ctx->fmt == 0) {
-        fac += (long long)s.NP * 2 * (s.W + 1);
-        ctx->sub_fbytes.push_back(8.0 * (double)s.N * (2.0 * s.w + 1.0));
-        const double kstop = 2.0 * s.nc * a_own;
-        ctx->sub_jbytes.push_back(8.0 * ((double)s.N * s.w + ((double)s.N - kstop) * (s.w + 1.0)));
-      } else {
+      {
         // the upper 16-tile triangle of W_a = S_a^{-1} P per line (block_line_doubles):
         // forward reads all nr, backward nr-1-a_stop of them
         const double blk = 8.0 * (double)block_line_doubles(s.NPS);
@@ -530,13 +513,6 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->pool_len = loc;
   ctx->fac_len = fac;
   ctx->ref_len = ref;
-  ctx->maxWS = ctx->maxW + NBF;
-  if (ctx->fmt == 0 && ctx->maxW > MAX_W) {   // the band format's compiled window
-    int code = fail(nullptr, OCP_ERR_UNSUPPORTED,
-                    "local half-bandwidth %d exceeds the compiled limit %d", ctx->maxW, MAX_W);
-    delete ctx;
-    return code;
-  }
   auto cleanup_fail = [&](int code) {
     g_global_err = ctx->err;
     ocp_ctx_destroy(ctx);
@@ -627,20 +603,10 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     CKC(gmalloc(&ctx->d_solve_order, I * sizeof(int)));
     CKC(cudaMemcpy(ctx->d_solve_order, sol.data(), I * sizeof(int), cudaMemcpyHostToDevice));
   }
-  // LU windows: up to 2 CTAs per SM, one (W+NB)^2 window each (L2 resident)
-  {
-    int per_sm = 2;
-    if (const char* e = getenv("OCP_LU_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));
-    ctx->lu_grid = std::min(I, per_sm * ctx->num_sms);
-  }
-  if (ctx->fmt == 0) {
-    ctx->ws_stride = (long long)ctx->maxWS * ctx->maxWS;
-    CKC(gmalloc(&ctx->scratch, ctx->lu_grid * ctx->ws_stride * sizeof(double)));
-  }
   // narrow lines (config 5): a 6-warp factor CTA, two per SM, when there
   // are enough subdomains to fill them and nearly every line fits its
   // 96-unknown shared-memory block (ocp_block_narrow.cu)
-  if (ctx->fmt == 1 && I >= 2 * ctx->num_sms) {
+  if (I >= 2 * ctx->num_sms) {
     int fit = 0;
     for (auto& sub : ctx->subs) fit += sub.pad_ <= narrow_factor_max_npb();
     ctx->bf_narrow = 10LL * fit >= 9LL * I;
@@ -648,12 +614,12 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   const int bf_per_sm = ctx->bf_narrow ? narrow_factor_ctas_per_sm() : 1;
   const int bf_max_npb = ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB;
   ctx->bf_grid = std::max(1, std::min(I, bf_per_sm * ctx->num_sms));
-  if (ctx->fmt == 1 && ctx->maxNPS > block_solve_max_nps()) {
+  if (ctx->maxNPS > block_solve_max_nps()) {
     fail(ctx, OCP_ERR_UNSUPPORTED, "local short side %d exceeds the block solve's limit %d",
          ctx->maxNPS / 2, block_solve_max_nps() / 2);
     return cleanup_fail(OCP_ERR_UNSUPPORTED);
   }
-  if (ctx->fmt == 1 && ctx->maxNPB > bf_max_npb) {
+  if (ctx->maxNPB > bf_max_npb) {
     // rows beyond the shared block, then (short side > 112) the line's
     // Jacobian diagonals (k_block_factor)
     ctx->bs_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4) + 2LL * ctx->maxNPB;
@@ -678,22 +644,7 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   {
     int optin = 0;
     CKC(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-    if (ctx->fmt == 0) {   // band format (OCP_FACTOR_FORMAT=band)
-      cudaFuncAttributes fa;
-      CKC(cudaFuncGetAttributes(&fa, k_band_factor));
-      if (factor_smem_bytes(ctx->maxW) + (int)fa.sharedSizeBytes > optin) {
-        fail(ctx, OCP_ERR_UNSUPPORTED, "LU panel needs more shared memory than the device offers");
-        return cleanup_fail(OCP_ERR_UNSUPPORTED);
-      }
-      CKC(raise_smem_limit((const void*)k_band_factor, factor_smem_bytes(ctx->maxW)));
-      const int solve_smem = (int)solve_smem_bytes(ctx->maxW);
-      if (solve_smem > optin) {
-        fail(ctx, OCP_ERR_UNSUPPORTED, "solve pipeline needs more shared memory than the device offers");
-        return cleanup_fail(OCP_ERR_UNSUPPORTED);
-      }
-      CKC(set_band_solve_smem(solve_smem));
-    }
-    if (ctx->fmt == 1) {
+    {
       // (lines wider than 224 unknowns use k_block_solve_wide, which sets its own limit)
       const int fb = block_factor_smem_bytes(ctx->maxNPB),
                 sb = (int)block_solve_smem_bytes(std::min(ctx->maxNPS, 224));
@@ -724,7 +675,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->scratch,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
@@ -1015,27 +966,13 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
   Timer tj(ctx, CLS_JVP);
-  if (ctx->fmt == 1) {   // one fused launch: rhs from d, solve, out[own] = -(d + x)
-    double bytes = 0;
-    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
-    Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(launch_block_solve(2, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
-                          ctx->P.off, ctx->maxNPS, d, out, ctx->P.n));
-    ++ctx->launches;
-    return OCP_OK;
-  }
-  const dim3 grid(I, 4);
-  k_jvp_rhs<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B);
-  CKL();
-  {
-    double bytes = 0;
-    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
-    Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(any_solve(ctx, 1, I, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B));
-    ++ctx->launches;
-  }
-  k_jvp_out<<<grid, 256, 0, st>>>(ctx->d_subs, ctx->P, d, ctx->B, out);
-  CKL();
+  // one fused launch: rhs from d, solve, out[own] = -(d + x)
+  double bytes = 0;
+  for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
+  Timer t(ctx, CLS_SOLVE, 0, bytes);
+  CK(launch_block_solve(2, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
+                        ctx->P.off, ctx->maxNPS, d, out, ctx->P.n));
+  ++ctx->launches;
   return OCP_OK;
 }
 
@@ -1296,26 +1233,13 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out)
   if (!ctx || !fac || !v || !out) return fail(ctx, OCP_ERR_ARG, "null argument");
   cudaStream_t st = ctx->stream;
   const int I = ctx->I;
-  if (ctx->fmt == 1) {   // one fused launch: rhs gathered per line, out[own] = x[own]
-    double bytes = 0;
-    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
-    Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(launch_block_solve(3, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
-                          ctx->P.off, ctx->maxNPS, v, out, ctx->P.n));
-    ++ctx->launches;
-    return OCP_OK;
-  }
-  k_gather<<<I, 256, 0, st>>>(ctx->d_subs, ctx->d_list_all, ctx->P, v, ctx->B);
-  CKL();
-  {
-    double bytes = 0;
-    for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
-    Timer t(ctx, CLS_SOLVE, 0, bytes);
-    CK(any_solve(ctx, 1, I, ctx->d_list_all, fac, ctx->B, 1.0, ctx->B));
-    ++ctx->launches;
-  }
-  k_ras_out<<<dim3(I, 4), 256, 0, st>>>(ctx->d_subs, ctx->P, ctx->B, out);
-  CKL();
+  // one fused launch: rhs gathered per line, out[own] = x[own]
+  double bytes = 0;
+  for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
+  Timer t(ctx, CLS_SOLVE, 0, bytes);
+  CK(launch_block_solve(3, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
+                        ctx->P.off, ctx->maxNPS, v, out, ctx->P.n));
+  ++ctx->launches;
   return OCP_OK;
 }
 

@@ -4,7 +4,6 @@
 //   k_global_residual  F_eps(x) on all n^2 points          system.py:147-152
 //   k_global_jacdiag   Jacobian diagonals + finite checks  system.py:135-144,155-160
 //   k_global_jvp       J(x) d, the CSR row sums of bmat    system.py:155-160
-//   k_ras_out          out[own_i] = z_i[own_in_local]       schwarz.py:234-239
 //   k_state_*          the semilinear state equation A y + phi(y) = f + u of
 //                      the manufactured problems (system.py:181-197, 257-265):
 //                      residual, diagonal of A + diag(phi'(y)), matrix-free CG
@@ -99,20 +98,6 @@ __global__ void __launch_bounds__(256) k_global_jvp(Phys P, const double4* __res
   }
 }
 
-// restricted prolongation of the local solutions: out[own_i] = z_i (band order)
-__global__ void k_ras_out(const SubInfo* subs, Phys P, const double* Zpool, double* out) {
-  const SubInfo s = subs[blockIdx.x];
-  const double2* Z = reinterpret_cast<const double2*>(Zpool + s.loc);
-  const long long Ntot = (long long)P.n * P.n;
-  const int oc = s.oc1 - s.oc0, cnt = (s.or1 - s.or0) * oc;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < cnt; e += gridDim.y * blockDim.x) {
-    const int i = s.or0 + e / oc, j = s.oc0 + e % oc;
-    const long long g = (long long)i * P.n + j;
-    const double2 z = Z[global_to_q(s, i, j)];
-    out[g] = z.x;
-    out[Ntot + g] = z.y;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // state equation (solve_state, system.py:181-197)

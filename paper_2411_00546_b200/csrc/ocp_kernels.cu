@@ -361,50 +361,7 @@ __global__ void k_scatter_fval(const SubInfo* subs, Phys P, const double* Vpool,
   }
 }
 
-// ---------------------------------------------------------------------------
-// JVP right-hand side e = [a_ext @ dy; a_ext @ dp] in band order
-// (schwarz.py:341-342); zero away from the ring
-// ---------------------------------------------------------------------------
-__global__ void k_jvp_rhs(const SubInfo* subs, Phys P, const double* d, double* Bpool) {
-  const SubInfo s = subs[blockIdx.x];
-  double2* B = reinterpret_cast<double2*>(Bpool + s.loc);
-  const long long Ntot = (long long)P.n * P.n;
-  const int n = P.n, npts = s.NP / 2, real = s.nr * s.nc;
-  for (int q = blockIdx.y * blockDim.x + threadIdx.x; q < npts; q += gridDim.y * blockDim.x) {
-    double ey = 0.0, ep = 0.0;
-    if (q < real) {
-      int i, j;
-      local_to_global(s, q / s.nc, q % s.nc, i, j);
-      const int di[4] = {-1, 0, 0, 1};
-      const int dj[4] = {0, -1, 1, 0};
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int ii = i + di[t], jj = j + dj[t];
-        if (ii < 0 || ii >= n || jj < 0 || jj >= n || in_rect(s, ii, jj)) continue;
-        const long long g = (long long)ii * n + jj;
-        ey = add(ey, mul(P.off, d[g]));
-        ep = add(ep, mul(P.off, d[Ntot + g]));
-      }
-    }
-    B[q] = make_double2(ey, ep);
-  }
-}
 
-// out[own] = -(d_loc + J^{-1} e)[own]   (schwarz.py:343-344)
-__global__ void k_jvp_out(const SubInfo* subs, Phys P, const double* d, const double* Zpool,
-                          double* out) {
-  const SubInfo s = subs[blockIdx.x];
-  const double2* Z = reinterpret_cast<const double2*>(Zpool + s.loc);
-  const long long Ntot = (long long)P.n * P.n;
-  const int oc = s.oc1 - s.oc0, cnt = (s.or1 - s.or0) * oc;
-  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < cnt; e += gridDim.y * blockDim.x) {
-    const int i = s.or0 + e / oc, j = s.oc0 + e % oc;
-    const long long g = (long long)i * P.n + j;
-    const double2 z = Z[global_to_q(s, i, j)];
-    out[g] = -add(d[g], z.x);
-    out[Ntot + g] = -add(d[Ntot + g], z.y);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // layout conversion between the reference local layout ([y_loc; p_loc],

@@ -31,9 +31,6 @@ __global__ void k_update(const SubInfo* subs, const int* list, double* Vpool, co
                          const double* alpha);
 __global__ void k_scatter_fval(const SubInfo* subs, Phys P, const double* Vpool, const double* x,
                                double* fval);
-__global__ void k_jvp_rhs(const SubInfo* subs, Phys P, const double* d, double* Bpool);
-__global__ void k_jvp_out(const SubInfo* subs, Phys P, const double* d, const double* Zpool,
-                          double* out);
 __global__ void k_ref_to_band(const SubInfo* subs, const double* ref, double* pool);
 __global__ void k_band_to_ref(const SubInfo* subs, const double* pool, double* ref);
 __global__ void k_dot(long long n, const double* x, const double* y, double* partials,
@@ -55,7 +52,6 @@ __global__ void k_global_residual(Phys P, const double* x, const double* f, cons
 __global__ void k_global_jacdiag(Phys P, const double* x, double eps, double4* JD,
                                  unsigned long long* bad);
 __global__ void k_global_jvp(Phys P, const double4* JD, const double* d, double* out);
-__global__ void k_ras_out(const SubInfo* subs, Phys P, const double* Zpool, double* out);
 __global__ void k_state_residual(Phys P, const double* y, const double* rhs, double* out);
 __global__ void k_state_diag(Phys P, const double* y, double* dg, unsigned long long* bad);
 __global__ void k_cg_ap(Phys P, const double* dg, const double* p, double* Ap, double* partials,
@@ -65,16 +61,6 @@ __global__ void k_cg_xr(long long N, const double* p, const double* Ap, double* 
 __global__ void k_cg_p(long long N, const double* r, double* p, const double* sc);
 __global__ void k_manufacture_yd(Phys P, const double* ybar, const double* pbar, double* yd);
 
-int factor_smem_bytes(int W);
-__global__ void k_band_factor(const SubInfo* subs, const int* list, int cnt, Phys P,
-                              const double* JDpool, double* fac_pool, double* scratch,
-                              long long ws_stride, int* status);
-// banded solve (ocp_solve.cu): mode 0 pool -> pool, mode 1 fused JVP
-size_t solve_smem_bytes(int max_w);
-cudaError_t launch_band_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
-                              const int* list, const double* fac, const double* in, double scale,
-                              double* out_pool, int max_w);
-cudaError_t set_band_solve_smem(int bytes);
 // block-tridiagonal format (ocp_block.cu)
 // Per line the store keeps the upper triangle of 16x16 tiles of
 // W_a = S_a^{-1} P (P swaps the y / p unknowns of every point; W_a is

@@ -10,7 +10,7 @@ repr, fields by ``%.17g``).  Every method runs on the device:
 * ``raspen`` / ``raspen-eps``      -> ``schwarz.raspen_solve``
 * ``newton-ras`` / ``newton-ras-eps`` -> ``linear_ras.newton_ras_solve``
 * ``newton`` / ``newton-eps``      -> monolithic Newton on the global residual;
-  ``linear_solver`` auto/direct: one banded LU of the whole Jacobian
+  ``linear_solver`` auto/direct: one block-Thomas factorisation of the whole Jacobian
   (single-subdomain engine, block factor of the whole grid), gmres: unpreconditioned
   device GMRES.
 
@@ -141,7 +141,7 @@ def schedule_for(cfg):
 
 def _monolithic(cfg, spec, sched, x0):
     """`experiments.py:86-91` on the device: direct solves on a single-subdomain
-    engine (one banded LU of the whole Jacobian), GMRES on a grid-only one."""
+    engine (one block-Thomas factorisation of the whole Jacobian), GMRES on a grid-only one."""
     if cfg.linear_solver in ("auto", "direct"):
         lin = "direct"
         engine = build_local_systems(decompose(spec.grid, 1, 1, 0), spec)

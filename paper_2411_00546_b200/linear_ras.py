@@ -11,8 +11,8 @@ left-preconditioned with one-level RAS rebuilt at every outer iterate
   reference's entry order
 * ``RasPreconditioner`` / ``ras_preconditioner`` / ``ras_precondition`` ->
   `schwarz.py:221-244`: the local pair Jacobians at ``x[pair_idx]`` go through
-  the same batched banded LU as RASPEN (kernel 2), the apply is the stored-factor
-  banded solve (kernel 4) + restricted prolongation
+  the same batched block-Thomas factor as RASPEN (kernel 2), the apply is the stored-factor
+  block solve (kernel 4) + restricted prolongation
 * ``newton_ras_solve`` -> the RAS branch of ``solve_single``; the direction
   solve runs as one native call (``ocp_ras_gmres``: JVP, RAS apply and MGS
   Arnoldi on the device, Givens on the host in the reference's order).
@@ -80,7 +80,7 @@ class GlobalJacobian:
 
     def direct_solve(self, rhs):
         """Sparse direct solve of J d = rhs (splu, `newton.py:125-129`): the
-        batched banded LU on a single-subdomain engine, i.e. one LU of the
+        batched block factor on a single-subdomain engine, i.e. one factorisation of the
         whole Jacobian (block-tridiagonal factor of 2n-unknown lines; any n up to
         1984, lines wider than 224 unknowns on the wide kernels)."""
         if self.engine.num_subdomains != 1:

@@ -4,7 +4,7 @@ Host side keeps what the reference keeps on the host: the tiling and index
 sets (`schwarz.py:78-126`), the outer Newton / GMRES control flow and the
 correction cache (`schwarz.py:348-411`).  Everything per subdomain - the
 frozen-exterior local residuals, the batched damped local Newton with eps
-continuation, in-kernel Jacobian assembly, banded LU factor/solve, the
+continuation, in-kernel Jacobian assembly, block-Thomas factor/solve, the
 refactorisation at the corrected values, the restricted prolongation and the
 stored-factor Jacobian action - runs in ``libocpgpu.so`` (one native call per
 RAS sweep, one per GMRES matvec).
@@ -12,7 +12,8 @@ RAS sweep, one per GMRES matvec).
 Differences from the reference that do not change results:
 * ``threads`` is accepted and ignored: all subdomains run batched on the GPU,
   deterministic by construction;
-* the local direct solves are a no-pivot banded LU instead of SuperLU (same
+* the local direct solves are a no-pivot block-Thomas elimination (stored
+  symmetric Schur inverses) instead of SuperLU (same
   solution to ~1e-13 relative, SURVEY.md 7);
 * the JVP evaluates ``-(d_loc + J^{-1} A_ext d)`` on the ownership block, which
   is algebraically the reference's ``-J^{-1}(J d_loc + A_ext d)``.

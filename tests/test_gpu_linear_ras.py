@@ -6,7 +6,7 @@ Fixtures: ``tests/golden/ras_*.npz`` from the unmodified reference
 Tolerances: the global residual and Jacobian action follow the reference's
 CSR entry order, so they are bitwise for the polynomial phi's and within a
 few ulps of the row scale where exp/pow enter (CUDA vs glibc libm).  The RAS
-preconditioner solves with a no-pivot banded LU instead of SuperLU: relative
+preconditioner solves with a no-pivot block-Thomas elimination instead of SuperLU: relative
 1e-10.  Solves: y/p/u within 1e-8 relative L2, outer iterations equal,
 GMRES iterations within +-1 per outer step.
 """

@@ -1,4 +1,4 @@
-"""Time the batched banded LU alone: the RAS-preconditioner factorisation of all
+"""Time the batched block factor alone: the RAS-preconditioner factorisation of all
 subdomains of a config (one k_band_factor launch per call)."""
 import sys
 
