@@ -125,9 +125,13 @@ constexpr int WLD = 33;
 #define OCP_LAW 4
 #endif
 constexpr int LAW = OCP_LAW;   // lookahead warps (0 .. LAW-1): the next pivot inverse while the others update
+// kmax: pivots kmax .. 31 of this block lie in the identity padding past the
+// line's n unknowns (decoupled: zero rows / columns outside the diagonal), so
+// their Gauss-Jordan steps are exact no-ops and are skipped - the last panel
+// of a 72-unknown line (NPB 96) takes 4 steps instead of 16.
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
-                                             int lane, int* bad) {
+                                             int lane, int* bad, int kmax) {
   // Gauss-Jordan with 2x2 pivot blocks: 16 dependent steps instead of 32.
   // Step s eliminates rows/columns K = {k, k+1}, k = 2s:
   //   S[K,K] <- P^{-1};  S[K,j] <- P^{-1} S[K,j];  S[i,K] <- -S[i,K] P^{-1};
@@ -142,7 +146,7 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   bool ok = true;
 #pragma unroll 1
-  for (int k = 0; k < 32; k += 2) {
+  for (int k = 0; k < kmax; k += 2) {
     const double* Wr = (k & 2) ? W1 : W0;
     double* Ww = (k & 2) ? W0 : W1;
     const double p00 = Wr[k * WLD + k], p01 = Wr[k * WLD + k + 1];
@@ -179,6 +183,11 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
 #pragma unroll
   for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
   if (!ok) *bad = 1;
+}
+// real pivots of the 32x32 pivot block at p0 (n even: 2x2 pivot pairs stay whole)
+__device__ __forceinline__ int pivot_kmax(int n, int p0) {
+  const int k = n - p0;
+  return k < 32 ? (k > 0 ? k : 0) : 32;
 }
 
 #ifdef OCP_DFMA_ONLY
@@ -434,7 +443,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     }
     if (grpA) {
       asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
-      pivot_inverse32<LAW>(R.row(0), lds, W0, W1, warp, lane, bad);
+      pivot_inverse32<LAW>(R.row(0), lds, W0, W1, warp, lane, bad, pivot_kmax(n, 0));
     }
     __syncthreads();
     BPH_MARK(1);
@@ -457,6 +466,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       // ---- P2: row block S[p, j] = Pinv S[p, j] (column tiles of 16 outside p)
       for (int tI = warp; tI < nct - 2; tI += NW) {
         const int j0 = 16 * (tI + (tI >= 2 * p ? 2 : 0));
+        if (j0 >= NPS) continue;   // identity padding: M[p, j] = 0 stays 0
         double c[4][2][2] = {};
         tile_32x16(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
         store_c(Prow + j0, lds, c, lane);
@@ -487,6 +497,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
         auto tile = [&](int tI) {
           int rt, ct;
           upper(tI, rt, ct);
+          if (16 * ct >= NPS) return;   // padding columns: M[p, j] = 0, no update
           double* Ci = R.row(32 * rt);
           double c[4][2][2];
           load_c(Ci + 16 * ct, lds, c, lane);
@@ -548,7 +559,8 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
             if (lrank < 2) tile(la0 + lrank);   // the two lookahead tiles
             asm volatile("bar.arrive 5, %0;" ::"n"(BF_THREADS) : "memory");
             asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
-            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad);
+            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad,
+                                 pivot_kmax(n, p0 + 32));
 #ifdef OCP_PHASE_TIMING
             if (tid == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tla));
 #endif
@@ -854,11 +866,13 @@ k_block_solve(const SubInfo* subs, const int* list, const double* fac_pool, cons
 // decompositions and the monolithic direct solve of newton[-eps]).
 // Warp w < NWC owns tile rows w, w + NWC, ... (TR of them, NWC <= 31);
 // the producer streams each tile column in units of G of its 16 columns
-// (G * (16c + 18) doubles <= WIDE_SBS), so any width fits the ring.  Row
+// (G * (16c + 18) doubles <= WIDE_SBS; G = 16 up to cpb = 32), so any width
+// fits the ring.  Row
 // and column parts are those of k_block_solve; tile columns are visited in
 // order 0 .. cpb-1 (two accumulators per row).
 // ---------------------------------------------------------------------------
-constexpr int WIDE_SBS = 4096;   // doubles per ring stage (32 KB)
+constexpr int WIDE_SBS = 8192;   // doubles per ring stage (64 KB): whole tile columns up to cpb = 32
+constexpr int WIDE_STAGES = 3;
 
 __host__ __device__ inline int wide_group(int cpb) {   // columns per unit
   int g = 16;
@@ -877,9 +891,9 @@ k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
   const int NPS = s.NPS, n = 2 * s.nc, nr = s.nr, cpb = NPS / 16;
   const int NWC = (cpb + TR - 1) / TR;                // consumer warps of this subdomain
   const int G = wide_group(cpb), upc = 16 / G, nunits = cpb * upc;
-  double* stage = sm;                                 // [BS_STAGES][WIDE_SBS]
-  double* vp = sm + BS_STAGES * WIDE_SBS;             // [2][max_nps]
-  __shared__ __align__(8) uint64_t full[BS_STAGES], empty[BS_STAGES];
+  double* stage = sm;                                 // [WIDE_STAGES][WIDE_SBS]
+  double* vp = sm + WIDE_STAGES * WIDE_SBS;             // [2][max_nps]
+  __shared__ __align__(8) uint64_t full[WIDE_STAGES], empty[WIDE_STAGES];
   const double* fac = fac_pool + s.fac;
   const double* in = in_pool + s.loc;
   double* out = out_pool + s.loc;
@@ -889,7 +903,7 @@ k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
   const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;
   const int nlines = nr + nback;
   if (tid == 0) {
-    for (int i = 0; i < BS_STAGES; ++i) {
+    for (int i = 0; i < WIDE_STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], NWC);
     }
@@ -904,14 +918,16 @@ k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
     if (lane == 0) {
       const long long total = (long long)nlines * nunits;
       for (long long t = 0; t < total; ++t) {
-        const int st = (int)(t % BS_STAGES);
-        if (t >= BS_STAGES) mbar_wait(&empty[st], (uint32_t)(((t / BS_STAGES) - 1) & 1));
+        const int st = (int)(t % WIDE_STAGES);
+        if (t >= WIDE_STAGES) mbar_wait(&empty[st], (uint32_t)(((t / WIDE_STAGES) - 1) & 1));
         const int blk = (int)(t / nunits), u = (int)(t % nunits);
         const int c = u / upc, q0 = (u % upc) * G, ld2 = 16 * c + 18;
         const double* src = fac + line_of(blk) * lsz + block_col_off(c, cpb) + (long long)q0 * ld2;
         const uint32_t bytes = (uint32_t)(8 * G * ld2);
         mbar_expect_tx(&full[st], bytes);
         bulk_g2s(stage + st * WIDE_SBS, src, bytes, &full[st]);
+        if (u == 0 && blk + 1 < nlines)   // the whole next line into L2 (short TMA latency)
+          bulk_prefetch_l2(fac + line_of(blk + 1) * lsz, (uint32_t)(8 * lsz));
       }
     }
     return;
@@ -954,7 +970,7 @@ k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      if (++st == BS_STAGES) { st = 0; ph ^= 1; }
+      if (++st == WIDE_STAGES) { st = 0; ph ^= 1; }
     }
 #pragma unroll
     for (int r = 0; r < TR; ++r) {
@@ -1000,7 +1016,7 @@ k_block_solve_wide(const SubInfo* subs, const int* list, const double* fac_pool,
 }
 
 size_t block_solve_wide_smem_bytes(int max_nps) {
-  return sizeof(double) * ((size_t)BS_STAGES * WIDE_SBS + 2 * (size_t)max_nps);
+  return sizeof(double) * ((size_t)WIDE_STAGES * WIDE_SBS + 2 * (size_t)max_nps);
 }
 
 template <int MODE>
