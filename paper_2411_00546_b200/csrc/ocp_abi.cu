@@ -70,6 +70,10 @@ struct ocp_ctx {
   long long bs_stride = 0;
   int bf_grid = 1;
   bool bf_narrow = false;     // narrow-line factor instance (ocp_block_narrow.cu)
+  int mc_K = 0;               // > 1: K CTAs per subdomain (k_block_factor_mc, few wide subdomains)
+  double* mscratch = nullptr; // their Schur blocks
+  long long ms_stride = 0;
+  unsigned long long* d_mcbars = nullptr;
   int num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
@@ -364,7 +368,14 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
     CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, (cnt + 1) * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
     const int grid = std::min(cnt, ctx->bf_grid);
-    if (ctx->bf_narrow) {
+    if (ctx->mc_K > 1) {   // few wide subdomains: K CTAs each (status / barriers zeroed first)
+      CK(cudaMemsetAsync(ctx->d_status, 0, ctx->I * sizeof(int), ctx->stream));
+      CK(cudaMemsetAsync(ctx->d_mcbars, 0, (size_t)16 * ctx->I * sizeof(unsigned long long),
+                         ctx->stream));
+      CK(launch_block_factor_mc(cnt, ctx->mc_K, ctx->stream, ctx->d_subs, ctx->d_flist, &ctx->P,
+                                ctx->JD, fac, ctx->mscratch, ctx->ms_stride, ctx->d_status,
+                                ctx->d_mcbars));
+    } else if (ctx->bf_narrow) {
       CK(launch_narrow_factor(grid, ctx->stream, ctx->d_subs, ctx->d_flist, cnt, &ctx->P, ctx->JD,
                               fac, ctx->bscratch, ctx->bs_stride, ctx->d_status));
     } else {
@@ -619,6 +630,17 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
          ctx->maxNPS / 2, block_solve_max_nps() / 2);
     return cleanup_fail(OCP_ERR_UNSUPPORTED);
   }
+  // few subdomains wider than the shared block: K CTAs per subdomain share its
+  // Schur block in global memory (k_block_factor_mc; OCP_FACTOR_MC=0 disables)
+  if (ctx->maxNPB > bf_max_npb && 2 * I <= ctx->num_sms) {
+    const char* e = getenv("OCP_FACTOR_MC");
+    if (!(e && e[0] == '0')) {
+      ctx->mc_K = std::min(32, ctx->num_sms / I);
+      ctx->ms_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
+      CKC(gmalloc(&ctx->mscratch, (size_t)I * ctx->ms_stride * sizeof(double)));
+      CKC(gmalloc(&ctx->d_mcbars, (size_t)16 * I * sizeof(unsigned long long)));
+    }
+  }
   if (ctx->maxNPB > bf_max_npb) {
     // rows beyond the shared block, then (short side > 112) the line's
     // Jacobian diagonals (k_block_factor)
@@ -675,7 +697,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->mscratch, (void*)ctx->d_mcbars,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,

@@ -643,6 +643,220 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
 
 int block_factor_threads() { return BF_THREADS; }
 
+#ifndef OCP_NARROW_INSTANCE
+// ---------------------------------------------------------------------------
+// k_block_factor_mc: the same factorisation, bitwise, for FEW WIDE subdomains
+// (coarse decompositions, the monolithic direct solve): K CTAs per subdomain
+// share its Schur block, which lives in global memory (L2).  Every phase of
+// the line / panel schedule of factor_one is split into independent items
+// (row pairs of the E phase, 32x16 DMMA tiles of P2 and P3a, transpose tasks
+// of P3b, stored columns) dealt round-robin to all warps of the K CTAs, with
+// a split arrival-counter barrier per subdomain between dependent phases:
+//   E | P1(0) | P2(0) | P3a(0) | P3b(0) + P1(1) | P2(1) | ... | P3b(last) |
+// (P1(p+1) touches only the pivot block p+1, P3b(p) only column block p).
+// Each item is computed exactly as factor_one computes it, so the stored
+// -W_a are identical to the single-CTA path's; only the schedule differs.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void mc_barrier(unsigned long long* ctr, unsigned long long& target,
+                                           int K) {
+  __syncthreads();
+  target += K;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BF_THREADS, 1)
+k_block_factor_mc(const SubInfo* subs, const int* list, int K, Phys P, const double* JDpool,
+                  double* fac_pool, double* mscratch, long long ms_stride, int* status,
+                  unsigned long long* bars) {
+  __shared__ double W0[32 * WLD], W1[32 * WLD];
+  __shared__ int bad;
+  const int li = blockIdx.x / K, rank = blockIdx.x - li * K;
+  const int sid = list[li];
+  const SubInfo s = subs[sid];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = BF_THREADS / 32;
+  const int gw = rank * NW + warp, GW = K * NW;   // this warp among all warps of the subdomain
+  const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr, lds = NPB + 4;
+  const int npan = NPB / 32, nct = NPB / 16, cpb = NPS / 16;
+  const double off = P.off, off2 = off * off;
+  const long long lsz = block_line_doubles(NPS);
+  const int nq = 4 * s.nc;
+  const double* JD = JDpool + 2 * s.loc;
+  double* fac = fac_pool + s.fac;
+  double* M = mscratch + (long long)li * ms_stride;
+  auto row = [&](int i) { return M + (long long)i * lds; };
+  unsigned long long* ctr = bars + 16 * li;   // one 128-byte line per subdomain
+  unsigned long long target = 0;
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  auto col_off = [cpb](int j) {
+    const int c = j >> 4;
+    return block_col_off(c, cpb) + (long long)(j - 16 * c) * (16 * c + 18);
+  };
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int a = 0; a < nr; ++a) {
+    const double* JL = JD + (long long)a * nq;   // this line's diagonals (global)
+    double* dstl = fac + (long long)(a - 1) * lsz;
+    // ---- E: row pairs (store line a-1's -W, rebuild M = P D_a - off^2 P W P)
+    for (int pi = gw; pi < NPB / 2; pi += GW) {
+      const int i0 = 2 * pi;
+      for (int cb = 0; cb < NPB; cb += 256) {
+        double2 v[2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = cb + 2 * lane + 64 * u;
+            v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(row(i0 + r) + j)
+                                         : make_double2(0.0, 0.0);
+          }
+        if (a > 0)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int i = i0 + r, m16 = 16 * (i >> 4) + 16;
+            if (i >= NPS) continue;
+            double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, cpb) +
+                                                      (long long)(i & 15) * (m16 + 2));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int j = cb + 2 * lane + 64 * u;
+              if (j < m16) __stcs(col + (j >> 1), v[r][u]);
+            }
+          }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int i = i0 + r;
+          double* rw = row(i);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = cb + 2 * lane + 64 * u;
+            if (j >= NPB) continue;
+            double2 w;
+            if (i < n && j < n) {
+              w.x = off2 * v[1 - r][u].y;
+              w.y = off2 * v[1 - r][u].x;
+            } else {
+              w.x = i == j ? 1.0 : 0.0;
+              w.y = i == j + 1 ? 1.0 : 0.0;
+            }
+            *reinterpret_cast<double2*>(rw + j) = w;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane < 14) {   // the seven diagonals of P D_a on the pair's two rows
+        const int i = i0 + lane / 7, j = i + lane % 7 - 3;
+        if (i < n && j >= 0 && j < n) row(i)[j] += d_entry(s, JL, i ^ 1, j, off);
+      }
+    }
+    mc_barrier(ctr, target, K);
+    // ---- P1 of panel 0
+    if (rank == 0 && warp < LAW)
+      pivot_inverse32<LAW>(row(0), lds, W0, W1, warp, lane, &bad, pivot_kmax(n, 0));
+    mc_barrier(ctr, target, K);
+    for (int p = 0; p < npan; ++p) {
+      const int p0 = 32 * p;
+      double* Prow = row(p0);
+      const double* Pinv = Prow + p0;
+      // ---- P2: row block tiles
+      for (int tI = gw; tI < nct - 2; tI += GW) {
+        const int j0 = 16 * (tI + (tI >= 2 * p ? 2 : 0));
+        if (j0 >= NPS) continue;
+        double c[4][2][2] = {};
+        tile_32x16(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
+        store_c(Prow + j0, lds, c, lane);
+      }
+      mc_barrier(ctr, target, K);
+      // ---- P3a: upper tiles outside panel p (factor_one's compact numbering)
+      {
+        const int total = p * (nct - 2) - p * (p - 1) + (npan - 1 - p) * nct -
+                          (npan - 1 - p) * (npan + p);
+        for (int tI = gw; tI < total; tI += GW) {
+          int rt, ct, t = tI;
+          for (rt = 0; rt < npan; ++rt) {
+            if (rt == p) continue;
+            const int cnt = nct - 2 * rt - (p > rt ? 2 : 0);
+            if (t < cnt) {
+              ct = 2 * rt + t;
+              if (p > rt && ct >= 2 * p) ct += 2;
+              break;
+            }
+            t -= cnt;
+          }
+          if (16 * ct >= NPS) continue;
+          double* Ci = row(32 * rt);
+          double c[4][2][2];
+          load_c(Ci + 16 * ct, lds, c, lane);
+          tile_32x16(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
+          store_c(Ci + 16 * ct, lds, c, lane);
+          if (ct >= 2 * rt + 2) {
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 2; ++ni)
+#pragma unroll
+                for (int k = 0; k < 2; ++k)
+                  row(16 * ct + 8 * ni + 2 * t4 + k)[32 * rt + 8 * mi + g] = c[mi][ni][k];
+          }
+        }
+      }
+      mc_barrier(ctr, target, K);
+      // ---- P3b of panel p (column block = row block transposed, pivot -A^{-1})
+      //      and P1 of panel p + 1 (disjoint data)
+      if (p + 1 < npan && rank == (p + 1) % K && warp < LAW)
+        pivot_inverse32<LAW>(row(p0 + 32) + p0 + 32, lds, W0, W1, warp, lane, &bad,
+                             pivot_kmax(n, p0 + 32));
+      for (int task = gw; task < 2 * (npan - 1); task += GW) {
+        int rt = task >> 1;
+        rt += rt >= p ? 1 : 0;
+        const int c0 = 16 * (task & 1), i = 32 * rt + lane;
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = Prow[(c0 + c) * lds + i];
+        double* dst = row(i) + p0 + c0;
+#pragma unroll
+        for (int c = 0; c < 16; c += 2)
+          *reinterpret_cast<double2*>(dst + c) = make_double2(v[c], v[c + 1]);
+      }
+      for (int e = gw * 32 + lane; e < 32 * 32; e += GW * 32) {
+        double* q = Prow + (e >> 5) * lds + p0 + (e & 31);
+        *q = -*q;
+      }
+      mc_barrier(ctr, target, K);
+    }
+  }
+  // the last line's -W: stored column j is the head of row j
+  double* dst = fac + (long long)(nr - 1) * lsz;
+  for (int j = gw; j < NPS; j += GW) {
+    const int m16 = 16 * (j >> 4) + 16;
+    for (int r = lane; r < m16; r += 32) __stcs(dst + col_off(j) + r, row(j)[r]);
+  }
+  __syncthreads();
+  if (tid == 0 && bad) atomicOr(&status[sid], 1);
+}
+
+cudaError_t launch_block_factor_mc(int cnt, int K, cudaStream_t st, const SubInfo* subs,
+                                   const int* list, const Phys* P, const double* JDpool,
+                                   double* fac_pool, double* mscratch, long long ms_stride,
+                                   int* status, unsigned long long* bars) {
+  Phys p = *P;
+  void* args[] = {(void*)&subs, (void*)&list, (void*)&K, (void*)&p, (void*)&JDpool,
+                  (void*)&fac_pool, (void*)&mscratch, (void*)&ms_stride, (void*)&status,
+                  (void*)&bars};
+  return cudaLaunchCooperativeKernel((void*)k_block_factor_mc, cnt * K, BF_THREADS, args, 0, st);
+}
+#endif
+
 int block_factor_smem_bytes(int max_npb) {
   (void)max_npb;   // fixed layout: [S: 160 x 164][W0, W1: 32 x 33][JL: 4 x 112]
   return (int)sizeof(double) * (BF_SMEM_MAX_NPB * (BF_SMEM_MAX_NPB + 4) + 2 * 32 * WLD + 4 * BF_JL_POINTS);

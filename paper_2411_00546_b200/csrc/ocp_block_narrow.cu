@@ -14,6 +14,7 @@
 #define OCP_LAW 2
 #define OCP_BF_MINB 2
 #define OCP_BF_SMEM_MAX_NPB 96
+#define OCP_NARROW_INSTANCE 1
 #define ocp ocp_nw
 #include "ocp_block.cu"
 #undef ocp

@@ -84,6 +84,11 @@ __global__ void k_block_factor(const SubInfo* subs, const int* list, int cnt, Ph
                                long long gs_stride, int* status);
 int block_factor_smem_bytes(int max_npb);
 int block_factor_threads();
+// few wide subdomains: K CTAs per subdomain (cooperative), Schur blocks in mscratch
+cudaError_t launch_block_factor_mc(int cnt, int K, cudaStream_t st, const SubInfo* subs,
+                                   const int* list, const Phys* P, const double* JDpool,
+                                   double* fac_pool, double* mscratch, long long ms_stride,
+                                   int* status, unsigned long long* bars);
 size_t block_solve_smem_bytes(int max_npb);
 int block_solve_max_nps();
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
