@@ -127,3 +127,24 @@ def test_monolithic_direct_newton_beyond_112_matches_reference():
         NewtonConfig(tol=1e-10, max_outer=200, sigma=1.1, linear_solver="direct"))
     assert rep.alphas == list(g["mono150_alphas"])
     _check(g, "mono150", cfg, x.to_host(), rep)
+
+
+def test_multi_cta_factor_is_bitwise_the_single_cta_factor(monkeypatch):
+    """k_block_factor_mc (K CTAs per wide subdomain, default for few
+    subdomains) stores exactly the single-CTA factor's -W_a: a RAS sweep and a
+    JVP agree bitwise with OCP_FACTOR_MC=0."""
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep
+    cfg, spec, _ = _problem("wide2x2")
+    out = {}
+    for mc in ("1", "0"):
+        monkeypatch.setenv("OCP_FACTOR_MC", mc)
+        dec = decompose(spec.grid, cfg.s1, cfg.s2, cfg.overlap)   # fresh engine
+        eng = build_local_systems(dec, spec)
+        x = eng.from_host(0.1 * np.random.default_rng(2).standard_normal(cfg.unknowns))
+        fac = eng.factor_store()
+        fval, inner = _sweep(eng, x, fac, ContinuationSchedule.fixed(1e-3), NewtonConfig(tol=1e-9))
+        d = eng.from_host(np.random.default_rng(3).standard_normal(cfg.unknowns))
+        out[mc] = (fval.to_host(), inner, _jvp(eng, fac, d).to_host())
+    assert out["1"][1] == out["0"][1]
+    np.testing.assert_array_equal(out["1"][0], out["0"][0])
+    np.testing.assert_array_equal(out["1"][2], out["0"][2])
