@@ -74,6 +74,8 @@ struct ocp_ctx {
   double* mscratch = nullptr; // their Schur blocks
   long long ms_stride = 0;
   unsigned long long* d_mcbars = nullptr;
+  int mc_Ks = 0;              // > 1: K CTAs per subdomain in the block solves (k_block_solve_mc)
+  double* mc_partials = nullptr;
   int num_sms = 148;
   double *red_partials = nullptr, *d_h = nullptr, *d_result = nullptr;
   unsigned int* red_counter = nullptr;
@@ -388,11 +390,27 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   }
 }
 
+// every block solve goes through here: K CTAs per subdomain for few wide
+// subdomains (k_block_solve_mc), else one CTA per subdomain
+cudaError_t solve_dispatch(ocp_ctx* ctx, int mode, int cnt, const int* d_list, const double* fac,
+                           const double* in, double scale, double* out_pool, const double* dglob,
+                           double* oglob) {
+  if (ctx->mc_Ks > 1) {
+    cudaError_t e = cudaMemsetAsync(ctx->d_mcbars, 0, (size_t)16 * ctx->I * sizeof(unsigned long long),
+                                    ctx->stream);
+    if (e != cudaSuccess) return e;
+    return launch_block_solve_mc(mode, cnt, ctx->mc_Ks, ctx->stream, ctx->d_subs, d_list, fac, in,
+                                 scale, out_pool, ctx->P.off, ctx->maxNPS, dglob, oglob, ctx->P.n,
+                                 ctx->mc_partials, ctx->d_mcbars);
+  }
+  return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out_pool,
+                            ctx->P.off, ctx->maxNPS, dglob, oglob, ctx->P.n);
+}
+
 cudaError_t any_solve(ocp_ctx* ctx, int mode, int cnt, const int* d_list, const double* fac,
                       const double* in, double scale, double* out) {
-  return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs,
-                            cnt == ctx->I ? ctx->d_solve_order : d_list, fac, in, scale, out,
-                            ctx->P.off, ctx->maxNPS);
+  return solve_dispatch(ctx, mode, cnt, cnt == ctx->I ? ctx->d_solve_order : d_list, fac, in, scale,
+                        out, nullptr, nullptr);
 }
 
 int launch_solve(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list, const double* fac,
@@ -639,6 +657,14 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
       ctx->ms_stride = (long long)ctx->maxNPB * (ctx->maxNPB + 4);
       CKC(gmalloc(&ctx->mscratch, (size_t)I * ctx->ms_stride * sizeof(double)));
       CKC(gmalloc(&ctx->d_mcbars, (size_t)16 * I * sizeof(unsigned long long)));
+      // the solves too when the lines are wider than the fast solve's 224 and
+      // fit k_block_solve_mc (NPS <= 496; at most 3 units of 8 columns per CTA)
+      const int units = 2 * (ctx->maxNPS / 16);
+      const int ks = std::min(ctx->mc_K, units);
+      if (ctx->maxNPS > 224 && ctx->maxNPS <= 496 && 3 * ks >= units) {
+        ctx->mc_Ks = ks;
+        CKC(gmalloc(&ctx->mc_partials, (size_t)I * 2 * ks * ctx->maxNPS * sizeof(double)));
+      }
     }
   }
   if (ctx->maxNPB > bf_max_npb) {
@@ -697,7 +723,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->mscratch, (void*)ctx->d_mcbars,
+                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->mscratch, (void*)ctx->d_mcbars, (void*)ctx->mc_partials,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
@@ -992,8 +1018,7 @@ int ocp_raspen_jvp(ocp_ctx* ctx, const double* fac, const double* d, double* out
   double bytes = 0;
   for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
   Timer t(ctx, CLS_SOLVE, 0, bytes);
-  CK(launch_block_solve(2, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
-                        ctx->P.off, ctx->maxNPS, d, out, ctx->P.n));
+  CK(solve_dispatch(ctx, 2, I, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B, d, out));
   ++ctx->launches;
   return OCP_OK;
 }
@@ -1259,8 +1284,7 @@ int ocp_ras_apply(ocp_ctx* ctx, const double* fac, const double* v, double* out)
   double bytes = 0;
   for (int i = 0; i < I; ++i) bytes += ctx->sub_jbytes[i];
   Timer t(ctx, CLS_SOLVE, 0, bytes);
-  CK(launch_block_solve(3, I, st, ctx->d_subs, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B,
-                        ctx->P.off, ctx->maxNPS, v, out, ctx->P.n));
+  CK(solve_dispatch(ctx, 3, I, ctx->d_solve_order, fac, nullptr, 1.0, ctx->B, v, out));
   ++ctx->launches;
   return OCP_OK;
 }

@@ -1261,6 +1261,166 @@ static cudaError_t launch_wide_mode(int grid, cudaStream_t st, const SubInfo* su
 
 int block_solve_max_nps() { return 16 * 31 * 8; }
 
+#ifndef OCP_NARROW_INSTANCE
+size_t block_solve_mc_smem_bytes(int max_nps);
+#endif
+
+#ifndef OCP_NARROW_INSTANCE
+// ---------------------------------------------------------------------------
+// k_block_solve_mc: the block solve for FEW WIDE subdomains, K CTAs per
+// subdomain (cooperative).  The stored tile columns of a line are split in
+// units of 8 columns, dealt round-robin to the K CTAs; each CTA streams its
+// units (TMA ring) and forms, for every row i, its partial of (-W_a v)[i]
+// (row parts of its columns, column parts of the stored columns it holds).
+// The partials go to a per-subdomain buffer, one arrival barrier per line,
+// and every CTA sums the K partials of all rows in rank order
+// (deterministic) and continues the forward / backward recurrence; rank 0
+// writes the outputs.  Rows: two threads each (one warp per tile row) + a
+// producer warp, so NPS <= 496.
+// ---------------------------------------------------------------------------
+constexpr int MC_UNIT_COLS = 8;
+constexpr int MC_SBS = 8 * (16 * 30 + 18) + 32;   // one unit of the widest tile column (NPS 496)
+constexpr int MC_STAGES = 6;
+
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1)
+k_block_solve_mc(const SubInfo* subs, const int* list, int K, const double* fac_pool,
+                 const double* in_pool, double scale, double* out_pool, double off, int max_nps,
+                 const double* dglob, double* oglob, int gn, double* partials,
+                 unsigned long long* bars) {
+  extern __shared__ __align__(16) double sm[];
+  const int li = blockIdx.x / K, rank = blockIdx.x - li * K;
+  const SubInfo s = subs[list[li]];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NPS = s.NPS, n = 2 * s.nc, nr = s.nr, cpb = NPS / 16;
+  const int upc = 16 / MC_UNIT_COLS, nunits = cpb * upc;
+  const int mine = nunits > rank ? (nunits - rank + K - 1) / K : 0;   // units of this CTA per line
+  double* stage = sm;                                  // [MC_STAGES][MC_SBS]
+  double* vp = sm + MC_STAGES * MC_SBS;                // [2][max_nps]
+  __shared__ __align__(8) uint64_t full[MC_STAGES], empty[MC_STAGES];
+  const double* fac = fac_pool + s.fac;
+  const double* in = in_pool + s.loc;
+  double* out = out_pool + s.loc;
+  const long long lsz = block_line_doubles(NPS);
+  double* part = partials + (long long)li * 2 * K * max_nps;   // [2][K][max_nps]
+  unsigned long long* ctr = bars + 16 * li;
+  unsigned long long target = 0;
+  int a_stop = 0;
+  if (MODE >= 1) a_stop = s.orient == 0 ? s.or0 - s.r0 : s.oc0 - s.c0;
+  const int nback = nr - 1 - a_stop > 0 ? nr - 1 - a_stop : 0;
+  const int nlines = nr + nback;
+  if (tid == 0) {
+    for (int i = 0; i < MC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], cpb);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = tid; t < NPS; t += blockDim.x)
+    vp[t ^ 1] = t < n ? (MODE == 2 ? jvp_rhs(s, dglob, gn, off, 0, t)
+                         : MODE == 3 ? ras_rhs(s, dglob, gn, 0, t) : scale * in[t]) : 0.0;
+  __syncthreads();
+  auto line_of = [&](int b) { return b < nr ? b : nr - 2 - (b - nr); };
+  const int nwarps = (int)(blockDim.x >> 5);
+  const bool producer = warp == nwarps - 1 && lane == 0;
+  long long tp = 0;   // producer's unit counter (ring slot = tp % MC_STAGES)
+  auto issue_line = [&](int blk) {   // this CTA's units of line blk (mine <= MC_STAGES / 2)
+    for (int k = 0; k < mine; ++k, ++tp) {
+      const int st = (int)(tp % MC_STAGES);
+      if (tp >= MC_STAGES) mbar_wait(&empty[st], (uint32_t)(((tp / MC_STAGES) - 1) & 1));
+      const int u = rank + K * k;
+      const int c = u / upc, q0 = (u % upc) * MC_UNIT_COLS, ld2 = 16 * c + 18;
+      const double* src = fac + line_of(blk) * lsz + block_col_off(c, cpb) + (long long)q0 * ld2;
+      const uint32_t bytes = (uint32_t)(8 * MC_UNIT_COLS * ld2);
+      mbar_expect_tx(&full[st], bytes);
+      bulk_g2s(stage + st * MC_SBS, src, bytes, &full[st]);
+    }
+  };
+  if (producer) issue_line(0);
+  const bool consumer = warp < cpb;
+  const int ti = warp, jj = lane & 15, h = lane >> 4, i = 16 * ti + jj;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int blk = 0; blk < nlines; ++blk) {
+    const bool fwd = blk < nr;
+    const int a = line_of(blk);
+    const double* v = vp + (blk & 1) * max_nps;
+    double* vnext = vp + ((blk + 1) & 1) * max_nps;
+    // this row's combine operand, read before the line's barrier (backward:
+    // rank 0 overwrites out[a] with x_a after it)
+    double nxt = 0.0;
+    if (consumer && h == 0 && i < n) {
+      if (fwd) {
+        if (a + 1 < nr)
+          nxt = MODE == 2 ? jvp_rhs(s, dglob, gn, off, a + 1, i)
+                : MODE == 3 ? ras_rhs(s, dglob, gn, a + 1, i) : in[(long long)(a + 1) * n + i];
+      } else {
+        nxt = out[(long long)a * n + i];
+      }
+    }
+    if (producer && blk + 1 < nlines) issue_line(blk + 1);
+    double p0 = 0.0, p1 = 0.0;
+    if (consumer) {
+      for (int k = 0; k < mine; ++k) {
+        const int u = rank + K * k;
+        const int c = u / upc, q0 = (u % upc) * MC_UNIT_COLS, ld2 = 16 * c + 18;
+        mbar_wait(&full[st], ph);
+        const double* cb = stage + st * MC_SBS;   // columns q0 .. q0+7 of tile column c
+        if (c >= ti && q0 == MC_UNIT_COLS * h) {   // row part: this thread's 8 columns
+#pragma unroll
+          for (int q = 0; q < MC_UNIT_COLS; q += 2) {
+            p0 = fma(cb[q * ld2 + i], v[16 * c + q0 + q], p0);
+            p1 = fma(cb[(q + 1) * ld2 + i], v[16 * c + q0 + q + 1], p1);
+          }
+        }
+        if (c == ti && jj >= q0 && jj < q0 + MC_UNIT_COLS) {   // column part
+          const double* cj = cb + (jj - q0) * ld2 + 2 * h;
+          const double* vr = v + 2 * h;
+          for (int r = 0; r < 16 * c; r += 4) {
+            const double2 x = *reinterpret_cast<const double2*>(cj + r);
+            const double2 y = *reinterpret_cast<const double2*>(vr + r);
+            p0 = fma(x.x, y.x, p0);
+            p1 = fma(x.y, y.y, p1);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (++st == MC_STAGES) { st = 0; ph ^= 1; }
+      }
+      double y = p0 + p1;
+      y += __shfl_xor_sync(0xffffffffu, y, 16);
+      if (h == 0) part[((long long)(blk & 1) * K + rank) * max_nps + i] = y;
+    }
+    mc_barrier(ctr, target, K);
+    if (consumer && h == 0) {
+      double y = 0.0;
+      for (int r = 0; r < K; ++r) y += __ldcg(part + ((long long)(blk & 1) * K + r) * max_nps + i);
+      y = -y;   // the store holds -W
+      double x = 0.0;
+      if (fwd) {
+        const double w = i < n ? y : 0.0;
+        if (rank == 0 && i < n && (MODE < 2 || a + 1 < nr)) out[(long long)a * n + i] = w;
+        vnext[i ^ 1] = (a + 1 < nr) ? (i < n ? fma(-off, w, scale * nxt) : 0.0) : w;
+        x = w;
+      } else {
+        x = i < n ? fma(-off, y, nxt) : 0.0;
+        if (rank == 0 && MODE < 2 && i < n) out[(long long)a * n + i] = x;
+        vnext[i ^ 1] = x;
+      }
+      if (rank == 0 && MODE >= 2 && (!fwd || a + 1 == nr) && i < n) {
+        int gi, gj;
+        local_to_global(s, a, i >> 1, gi, gj);
+        if (gi >= s.or0 && gi < s.or1 && gj >= s.oc0 && gj < s.oc1) {
+          const long long g = (long long)(i & 1) * gn * gn + (long long)gi * gn + gj;
+          oglob[g] = MODE == 2 ? -add(dglob[g], x) : x;
+        }
+      }
+    }
+    __syncthreads();   // vnext complete; (backward) out[a] read before the next line writes
+  }
+}
+#endif
+
 size_t block_solve_smem_bytes(int max_npb) {
   return sizeof(double) * ((size_t)BS_STAGES * bs_stage_doubles(max_npb) + 2 * (size_t)max_npb);
 }
@@ -1303,5 +1463,31 @@ cudaError_t set_block_kernel_smem(int factor_bytes, int solve_bytes) {
   if (e != cudaSuccess) return e;
   return raise_smem_limit((const void*)k_block_solve<3>, solve_bytes);
 }
+
+#ifndef OCP_NARROW_INSTANCE
+size_t block_solve_mc_smem_bytes(int max_nps) {
+  return sizeof(double) * ((size_t)MC_STAGES * MC_SBS + 2 * (size_t)max_nps);
+}
+
+// K CTAs per subdomain; partials: [cnt][2][K][max_nps] doubles, bars: 16 per subdomain (zeroed)
+cudaError_t launch_block_solve_mc(int mode, int cnt, int K, cudaStream_t st, const SubInfo* subs,
+                                  const int* list, const double* fac, const double* in,
+                                  double scale, double* out_pool, double off, int max_nps,
+                                  const double* dglob, double* oglob, int gn, double* partials,
+                                  unsigned long long* bars) {
+  const int cpb = max_nps / 16;
+  const int nt = 32 * (cpb + 1);
+  if (nt > 1024) return cudaErrorInvalidConfiguration;
+  const size_t smem = block_solve_mc_smem_bytes(max_nps);
+  void* fn = mode == 0 ? (void*)k_block_solve_mc<0> : mode == 1 ? (void*)k_block_solve_mc<1>
+           : mode == 2 ? (void*)k_block_solve_mc<2> : (void*)k_block_solve_mc<3>;
+  cudaError_t e = raise_smem_limit((const void*)fn, (int)smem);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&subs, (void*)&list, (void*)&K, (void*)&fac, (void*)&in, (void*)&scale,
+                  (void*)&out_pool, (void*)&off, (void*)&max_nps, (void*)&dglob, (void*)&oglob,
+                  (void*)&gn, (void*)&partials, (void*)&bars};
+  return cudaLaunchCooperativeKernel(fn, cnt * K, nt, args, smem, st);
+}
+#endif
 
 }  // namespace ocp

@@ -91,6 +91,12 @@ cudaError_t launch_block_factor_mc(int cnt, int K, cudaStream_t st, const SubInf
                                    int* status, unsigned long long* bars);
 size_t block_solve_smem_bytes(int max_npb);
 int block_solve_max_nps();
+// few wide subdomains: K CTAs per subdomain (cooperative), one barrier per line
+cudaError_t launch_block_solve_mc(int mode, int cnt, int K, cudaStream_t st, const SubInfo* subs,
+                                  const int* list, const double* fac, const double* in,
+                                  double scale, double* out_pool, double off, int max_nps,
+                                  const double* dglob, double* oglob, int gn, double* partials,
+                                  unsigned long long* bars);
 cudaError_t launch_block_solve(int mode, int grid, cudaStream_t st, const SubInfo* subs,
                                const int* list, const double* fac, const double* in, double scale,
                                double* out_pool, double off, int max_npb,
