@@ -207,7 +207,8 @@ def run_ours(args):
     dist = Dist("nccl")
     import torch
     torch.cuda.set_device(dist.local)
-    from paper_2411_00546_b200 import KrylovConfig, NewtonConfig, build_local_systems, raspen_solve
+    from paper_2411_00546_b200 import (ContinuationSchedule, KrylovConfig, NewtonConfig,
+                                       build_local_systems, raspen_solve)
     from paper_2411_00546_b200.schwarz import release_local_systems, solve_on_device
     from paper_2411_00546_b200.system import ProblemSpec
 
@@ -275,6 +276,32 @@ def run_ours(args):
             del fresh, x
             gc.collect()   # outside the timed region: the step's engine is torn down now
     e2e_step = dist.max(statistics.mean(e2e_ms)) if e2e_ms else None
+
+    # the same quantity as cpu_baseline / --impl reference, end to end: the
+    # first RAS evaluation (x = 0, eps continuation) through the public
+    # raspen_residual on host arrays (x in; f_val and every local value out)
+    e2e_sweep = None
+    if not args.no_e2e:
+        from paper_2411_00546_b200 import raspen_residual
+        inner_cfg = NewtonConfig(tol=INNER_TOL, max_outer=200)
+        esched = ContinuationSchedule(cfg.eps0, cfg.gamma, cfg.eps_min)
+        sw_ms, sw_dof = [], 0.0
+        for it in range(args.steps + 1):
+            dist.barrier()
+            t0 = time.perf_counter()
+            f_val, corr = raspen_residual(x0, dec, spec, cfg.eps_min, inner_cfg, esched)
+            if it > 0:
+                sw_ms.append((time.perf_counter() - t0) * 1e3)
+            sw_dof = float(sum(2 * s.size * k for s, k in zip(dec.subdomains, corr.inner_iters)))
+            del f_val, corr
+        sw = dist.max(statistics.mean(sw_ms))
+        e2e_sweep = {"value": dist.sum(sw_dof) / (sw / 1e3), "unit": UNIT, "ms_per_step": sw,
+                     "dof_updates": sw_dof,
+                     "h2d_bytes_per_step": 8 * cfg.unknowns,
+                     "d2h_bytes_per_step": 8 * cfg.unknowns + 8 * sum(2 * s.size for s in dec.subdomains),
+                     "definition": "first RAS evaluation (x=0, eps 1->1e-6) through the public "
+                                   "raspen_residual on host arrays: the quantity cpu_baseline and "
+                                   "--impl reference time on the CPU"}
 
     # roofline of the dominant kernels (per-launch averages over the timed region)
     peaks = load_peaks()
@@ -366,6 +393,7 @@ def run_ours(args):
                 "ms_per_step": e2e_step,
                 "timer": "host perf_counter around raspen_solve(host x0) incl. context build",
                 "definition": "DOF-updates / whole e2e solve time (conservative vs value)"},
+        "e2e_sweep": e2e_sweep,
         "gpu_launches": int(st["launches"]),
         "clocks": clocks,
         "stress_config5": stress,
