@@ -1,5 +1,5 @@
 """Time the batched block factor alone: the RAS-preconditioner factorisation of all
-subdomains of a config (one k_band_factor launch per call)."""
+subdomains of a config (one k_block_factor launch per call)."""
 import sys
 
 import numpy as np

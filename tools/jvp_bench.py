@@ -1,5 +1,5 @@
 """Time the stored-factor JVP solve alone at a config (after one RAS sweep):
-average k_block_solve<1> + rhs/out launch time from the context's CUDA-event
+average fused k_block_solve<2> launch time from the context's CUDA-event
 stats.  OCP_LIB selects an experiment build of libocpgpu.so."""
 import os
 import sys

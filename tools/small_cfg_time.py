@@ -1,3 +1,4 @@
+"""Wall time and kernel split of the small BASELINE configs 1 and 2 (latency-bound solves)."""
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")

@@ -1,4 +1,4 @@
-"""Config-5 stress timing alone (bench.stress_config5); OCP_FACTOR_FORMAT selects the factor format."""
+"""Config-5 stress timing alone (bench.stress_config5)."""
 import sys, json
 sys.path.insert(0, ".")
 sys.argv = ["bench.py"]

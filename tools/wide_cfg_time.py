@@ -1,3 +1,4 @@
+"""Wall time and kernel split of the wide2x2 decomposition (300^2, 2x2: local short side 158)."""
 import sys, time
 import numpy as np
 sys.path.insert(0, ".")
