@@ -125,7 +125,7 @@ def test_guard_zones_and_repeat_determinism():
     import subprocess
     import sys
     env = dict(os.environ, OCP_GUARD="1", OCP_REPEAT="5")
-    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sanitize_run.py"), "--all"],
+    out = subprocess.run([sys.executable, os.path.join(REPO, "tools", "sanitize_run.py"), "--all", "--wide"],
                          env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert "corrupted_bytes=0" in out.stdout

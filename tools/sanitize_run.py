@@ -67,6 +67,32 @@ if "--big" in sys.argv:   # oversized-block paths: config 4 (n = 172 corner), co
         del out, fval, fac, xd, eng
         release_local_systems(dc)
 
+if "--wide" in sys.argv:   # wide lines: k_block_factor_mc, k_block_solve_mc, k_block_solve_wide
+    from paper_2411_00546_b200 import build_local_systems, newton_continuation
+    from paper_2411_00546_b200.linear_ras import GlobalJacobian, global_residual
+    from paper_2411_00546_b200.problems import EXTRA_CONFIGS
+    c = EXTRA_CONFIGS["wide2x2"]
+    sp_ = build_spec(c, with_matrix=False)
+    dc = decompose(sp_.grid, c.s1, c.s2, c.overlap)
+    x, rep = raspen_solve(np.zeros(c.unknowns), dc, sp_, ContinuationSchedule(c.eps0, c.gamma, c.eps_min),
+                          cfg=NewtonConfig(tol=1e-10), krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000),
+                          inner_tol=1e-8)
+    print("wide2x2 raspen:", rep.converged, rep.outer_iters, rep.gmres_iters, flush=True)
+    os.environ["OCP_FACTOR_MC"] = "0"   # the single-CTA wide kernels too
+    dc2 = decompose(sp_.grid, c.s1, c.s2, c.overlap)
+    x2, rep2 = raspen_solve(np.zeros(c.unknowns), dc2, sp_, ContinuationSchedule(c.eps0, c.gamma, c.eps_min),
+                            cfg=NewtonConfig(tol=1e-10), krylov_cfg=KrylovConfig(rel_tol=1e-8, max_iters=1000),
+                            inner_tol=1e-8)
+    print("wide2x2 raspen (single-CTA wide kernels):", rep2.converged, rep2.outer_iters, flush=True)
+    del os.environ["OCP_FACTOR_MC"]
+    c = EXTRA_CONFIGS["mono150"]
+    sp_ = build_spec(c, with_matrix=False)
+    e = build_local_systems(decompose(sp_.grid, 1, 1, 0), sp_)
+    x, rep = newton_continuation(e.from_host(np.zeros(c.unknowns)), lambda x, ep: global_residual(e, x, ep),
+                                 lambda x, ep: GlobalJacobian(e, x, ep), ContinuationSchedule(1.0, 0.1, 1e-6),
+                                 NewtonConfig(tol=1e-10, linear_solver="direct"))
+    print("mono150 direct:", rep.converged, rep.outer_iters, flush=True)
+
 # racecheck stand-in: the same solves repeated must be bitwise identical
 # (mbarrier rings, named barriers, grid barrier and tickets all feed
 # fixed-order reductions, so any race shows up as a changed bit)
