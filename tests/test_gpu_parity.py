@@ -530,3 +530,47 @@ def test_device_gmres_on_the_global_jacobian_matches_oracle():
     assert got.iters == ko and got.converged == cvo
     assert np.max(np.abs(np.array(got.history) - np.array(ho)) / ho[0]) <= 1e-10
     assert rel_l2(got.x.to_host(), do) <= 1e-9
+
+
+def test_local_correction_ignores_other_subdomains_failures():
+    """With an inner iteration budget that only some subdomains meet,
+    raspen_residual raises the lowest failing subdomain (the reference's
+    thread-pool map), while local_correction(i) of a subdomain within the
+    budget returns its values (`schwarz.py:211-218` solves i alone)."""
+    from paper_2411_00546_b200 import local_correction
+    tag, n, s1, s2, m, phi, nu, mu = UNIT_CASES[1]
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, s1, s2, m)
+    prob = O.Problem(n, s1, s2, m, phi, nu, mu, spec.f, spec.y_d)
+    x = 0.3 * np.random.default_rng(17).standard_normal(2 * n * n)
+    sched = ContinuationSchedule(1.0, 0.2, 1e-2)
+    counts = [prob.local_solve(i, x, 1.0, 0.2, 1e-2, 1e-10, 200)[1] for i in range(len(dec))]
+    budget = min(counts)
+    assert max(counts) > budget, counts   # some subdomain needs more than the budget
+    ok = counts.index(budget)
+    cfg = NewtonConfig(tol=1e-10, max_outer=budget)
+    with pytest.raises(LocalSolveError) as exc:
+        raspen_residual(x, dec, spec, 1e-2, inner_cfg=cfg, inner_sched=sched)
+    assert exc.value.subdomain == next(i for i, c in enumerate(counts) if c > budget)
+    v = local_correction(ok, x, dec, spec, 1e-2, inner_cfg=cfg, inner_sched=sched)
+    vo, _ = prob.local_solve(ok, x, 1.0, 0.2, 1e-2, 1e-10, budget)
+    assert rel_l2(v, vo) <= 1e-10
+
+
+@pytest.mark.parametrize("n,s1,s2,m", [(4, 2, 2, 0), (5, 2, 1, 1), (7, 3, 3, 1), (9, 1, 3, 2), (6, 1, 1, 0)])
+def test_tiny_grids_residual_and_jvp_match_oracle(n, s1, s2, m):
+    """Edge cases of the tiling: tiny grids, zero overlap, 1-wide owned tiles,
+    single subdomain - RAS residual and JVP against the oracle."""
+    phi, nu, mu = make_phi("cubic"), 1e-3, 1e-2
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, s1, s2, m)
+    prob = O.Problem(n, s1, s2, m, phi, nu, mu, spec.f, spec.y_d)
+    rng = np.random.default_rng(n * 10 + s1)
+    x = 0.2 * rng.standard_normal(2 * n * n)
+    f_val, corr = raspen_residual(x, dec, spec, 1e-2, inner_cfg=NewtonConfig(tol=1e-11))
+    fo, co = O.raspen_residual(prob, x, 1e-2, tol=1e-11, threads=1)
+    assert corr.inner_iters == list(co.inner)
+    assert rel_l2(f_val, fo) <= 1e-10
+    d = rng.standard_normal(x.shape[0])
+    out = raspen_jacobian_apply(x, d, dec, spec, 1e-2, corr)
+    assert rel_l2(out, O.raspen_jvp(prob, x, d, 1e-2, co)) <= 1e-10
