@@ -374,9 +374,15 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
       CK(cudaMemsetAsync(ctx->d_status, 0, ctx->I * sizeof(int), ctx->stream));
       CK(cudaMemsetAsync(ctx->d_mcbars, 0, (size_t)16 * ctx->I * sizeof(unsigned long long),
                          ctx->stream));
-      CK(launch_block_factor_mc(cnt, ctx->mc_K, ctx->stream, ctx->d_subs, ctx->d_flist, &ctx->P,
-                                ctx->JD, fac, ctx->mscratch, ctx->ms_stride, ctx->d_status,
-                                ctx->d_mcbars));
+      cudaError_t e = launch_block_factor_mc(cnt, ctx->mc_K, ctx->stream, ctx->d_subs, ctx->d_flist,
+                                             &ctx->P, ctx->JD, fac, ctx->mscratch, ctx->ms_stride,
+                                             ctx->d_status, ctx->d_mcbars);
+      if (e == cudaErrorCooperativeLaunchTooLarge) {   // SMs taken: one CTA per subdomain from now on
+        cudaGetLastError();
+        ctx->mc_K = ctx->mc_Ks = 0;
+        return launch_factor(ctx, d_list, list, fac);
+      }
+      CK(e);
     } else if (ctx->bf_narrow) {
       CK(launch_narrow_factor(grid, ctx->stream, ctx->d_subs, ctx->d_flist, cnt, &ctx->P, ctx->JD,
                               fac, ctx->bscratch, ctx->bs_stride, ctx->d_status));
@@ -399,9 +405,12 @@ cudaError_t solve_dispatch(ocp_ctx* ctx, int mode, int cnt, const int* d_list, c
     cudaError_t e = cudaMemsetAsync(ctx->d_mcbars, 0, (size_t)16 * ctx->I * sizeof(unsigned long long),
                                     ctx->stream);
     if (e != cudaSuccess) return e;
-    return launch_block_solve_mc(mode, cnt, ctx->mc_Ks, ctx->stream, ctx->d_subs, d_list, fac, in,
-                                 scale, out_pool, ctx->P.off, ctx->maxNPS, dglob, oglob, ctx->P.n,
-                                 ctx->mc_partials, ctx->d_mcbars);
+    e = launch_block_solve_mc(mode, cnt, ctx->mc_Ks, ctx->stream, ctx->d_subs, d_list, fac, in,
+                              scale, out_pool, ctx->P.off, ctx->maxNPS, dglob, oglob, ctx->P.n,
+                              ctx->mc_partials, ctx->d_mcbars);
+    if (e != cudaErrorCooperativeLaunchTooLarge) return e;
+    cudaGetLastError();   // SMs taken: one CTA per subdomain from now on
+    ctx->mc_Ks = 0;
   }
   return launch_block_solve(mode, cnt, ctx->stream, ctx->d_subs, d_list, fac, in, scale, out_pool,
                             ctx->P.off, ctx->maxNPS, dglob, oglob, ctx->P.n);
