@@ -56,9 +56,8 @@ struct ocp_ctx {
   double *d_f = nullptr, *d_yd = nullptr;
   double *V = nullptr, *R = nullptr, *D = nullptr, *B = nullptr, *JD = nullptr;
   int *d_list_all = nullptr, *d_list = nullptr, *d_status = nullptr, *d_flags = nullptr;
-  double *d_alpha = nullptr, *d_norm2 = nullptr, *d_rpart = nullptr;
+  double *d_alpha = nullptr, *d_rpart = nullptr;   // d_rpart: per (subdomain, residual CTA) squared-norm partial
   unsigned long long* d_rbad = nullptr;   // per (subdomain, residual CTA) first bad phi'/phi
-  unsigned int* d_rcount = nullptr;
   int res_chunks = 1;
   int res_smem = 0;           // dynamic shared memory of k_residual
   long long* d_bad = nullptr;
@@ -100,7 +99,10 @@ struct ocp_ctx {
   int h_cap = 0;
   cudaStream_t stream = nullptr;
   // pinned host staging
-  double* h_norm2 = nullptr;
+  double* h_norm2 = nullptr;   // squared residual norms per subdomain (finish_residual)
+  double* h_rpart = nullptr;   // pinned: per-CTA partials of the last residual
+  unsigned long long* h_rbad = nullptr;
+  std::vector<long long> res_bad;   // first nonfinite phi'/phi'' key of the last residual with Jacobian diagonals
   int* h_status = nullptr;
   long long* h_bad = nullptr;
   int* h_list = nullptr;
@@ -325,16 +327,47 @@ int launch_residual(ocp_ctx* ctx, const int* d_list, int cnt, const double* x, c
   // full-set residual evaluations are timed for the stencil roofline
   // (48 B per local point: read y,p,f,y_d, write r1,r2 - SURVEY.md 8d; with
   // the fused Jacobian diagonals 80 B: + the (dg, b12, b21, 0) write)
+  {
   Timer t(cnt == ctx->I && !D ? ctx : nullptr, CLS_RESID, 0,
           ctx->resid_bytes_all * (jd ? 80.0 / 48.0 : 1.0));
   const dim3 grid(cnt, ctx->res_chunks);
   // every list is an ascending subset of the subdomains, so a full-count
   // list is the identity: the kernel then skips the list indirection
-  k_residual<<<grid, RES_THREADS, ctx->res_smem, ctx->stream>>>(
-      ctx->d_subs, cnt == ctx->I ? nullptr : d_list, ctx->P, x, V, D, alpha, ctx->d_f, ctx->d_yd, eps, R, ctx->d_norm2,
-      ctx->d_rpart, ctx->d_rcount, jd ? ctx->JD : nullptr, ctx->d_rbad, ctx->d_bad);
+  if (!D)   // no staged direction: the compact L1-read path
+    k_residual<true><<<grid, RES_THREADS, 0, ctx->stream>>>(
+        ctx->d_subs, cnt == ctx->I ? nullptr : d_list, ctx->P, x, V, D, alpha, ctx->d_f, ctx->d_yd, eps, R,
+        ctx->d_rpart, jd ? ctx->JD : nullptr, ctx->d_rbad);
+  else
+  k_residual<false><<<grid, RES_THREADS, ctx->res_smem, ctx->stream>>>(
+      ctx->d_subs, cnt == ctx->I ? nullptr : d_list, ctx->P, x, V, D, alpha, ctx->d_f, ctx->d_yd, eps, R,
+      ctx->d_rpart, jd ? ctx->JD : nullptr, ctx->d_rbad);
   CKL();
+  }
+  // the per-CTA partials come back with the copy the caller waits for anyway
+  const size_t np = (size_t)ctx->I * ctx->res_chunks;
+  CK(cudaMemcpyAsync(ctx->h_rpart, ctx->d_rpart, np * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (jd)
+    CK(cudaMemcpyAsync(ctx->h_rbad, ctx->d_rbad, np * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
   return OCP_OK;
+}
+
+// after the stream synchronisation that follows launch_residual: squared norms
+// of the listed subdomains (partials added in CTA order: deterministic) and,
+// for a residual with Jacobian diagonals, their first nonfinite phi' / phi'' key
+void finish_residual(ocp_ctx* ctx, const int* list, int cnt, bool jd) {
+  const int ny = ctx->res_chunks;
+  for (int k = 0; k < cnt; ++k) {
+    const int i = list ? list[k] : k;
+    double v = 0.0;
+    for (int y = 0; y < ny; ++y) v += ctx->h_rpart[(size_t)i * ny + y];
+    ctx->h_norm2[i] = v;
+    if (jd) {
+      unsigned long long b = ~0ull;
+      for (int y = 0; y < ny; ++y) b = std::min(b, ctx->h_rbad[(size_t)i * ny + y]);
+      ctx->res_bad[i] = b == ~0ull ? -1ll : (long long)b;
+    }
+  }
 }
 
 int upload_list(ocp_ctx* ctx, const std::vector<int>& list) {
@@ -597,7 +630,6 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   CKC(gmalloc(&ctx->d_list, I * sizeof(int)));
   CKC(gmalloc(&ctx->d_status, I * sizeof(int)));
   CKC(gmalloc(&ctx->d_alpha, I * sizeof(double)));
-  CKC(gmalloc(&ctx->d_norm2, I * sizeof(double)));
   {
     // residual grid: one CTA per RQ consecutive local points, staging the
     // points plus one local row either side in dynamic shared memory
@@ -608,12 +640,10 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
     }
     ctx->res_chunks = maxt;
     ctx->res_smem = (int)residual_smem_bytes(max_nc);
-    CKC(raise_smem_limit((const void*)k_residual, ctx->res_smem));
+    CKC(raise_smem_limit((const void*)k_residual<false>, ctx->res_smem));
   }
   CKC(gmalloc(&ctx->d_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
   CKC(gmalloc(&ctx->d_rbad, (size_t)I * ctx->res_chunks * sizeof(unsigned long long)));
-  CKC(gmalloc(&ctx->d_rcount, I * sizeof(unsigned int)));
-  CKC(cudaMemset(ctx->d_rcount, 0, I * sizeof(unsigned int)));
   CKC(gmalloc(&ctx->d_bad, I * sizeof(long long)));
   CKC(gmalloc(&ctx->d_flags, 4 * sizeof(int)));
   {
@@ -692,6 +722,9 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->h_cap = 4096;
   CKC(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_norm2, I * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
+  CKC(cudaMallocHost(&ctx->h_rbad, (size_t)I * ctx->res_chunks * sizeof(unsigned long long)));
+  ctx->res_bad.assign(I, -1ll);
   CKC(cudaMallocHost(&ctx->h_status, I * sizeof(int)));
   CKC(cudaMallocHost(&ctx->h_bad, I * sizeof(long long)));
   CKC(cudaMallocHost(&ctx->h_list, I * sizeof(int)));
@@ -732,14 +765,14 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   for (void* p : {(void*)ctx->d_subs, (void*)ctx->d_f, (void*)ctx->d_yd, (void*)ctx->V, (void*)ctx->R,
                   (void*)ctx->D, (void*)ctx->B, (void*)ctx->JD, (void*)ctx->d_list_all,
                   (void*)ctx->d_list, (void*)ctx->d_status, (void*)ctx->d_alpha,
-                  (void*)ctx->d_norm2, (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_rcount, (void*)ctx->d_flags, (void*)ctx->mscratch, (void*)ctx->d_mcbars, (void*)ctx->mc_partials,
+                  (void*)ctx->d_bad, (void*)ctx->d_rpart, (void*)ctx->d_rbad, (void*)ctx->d_flags, (void*)ctx->mscratch, (void*)ctx->d_mcbars, (void*)ctx->mc_partials,
                   (void*)ctx->red_partials, (void*)ctx->red_counter, (void*)ctx->arn_bar, (void*)ctx->arn_partials, (void*)ctx->d_result,
                   (void*)ctx->gm_Q, (void*)ctx->gm_w, (void*)ctx->gm_dh, (void*)ctx->gm_t,
                   (void*)ctx->st_buf, (void*)ctx->st_sc, (void*)ctx->st_hist,
                   (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist, (void*)ctx->d_solve_order,
                   (void*)ctx->d_h})
     if (p) gfree(p);
-  for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
+  for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_rpart, (void*)ctx->h_rbad, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
                   (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
                   (void*)ctx->gm_hh, (void*)ctx->st_hhist, (void*)ctx->h_flist})
     if (p) cudaFreeHost(p);
@@ -851,8 +884,8 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
   // the first residual also produces the Jacobian diagonals at eps0
   if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->V, nullptr, nullptr, eps, ctx->R, true))
     return rc;
-  CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  finish_residual(ctx, nullptr, I, true);
   for (int i = 0; i < I; ++i) {
     if (only >= 0 && i != only) {   // local_correction: subdomain `only` alone
       state[i] = DONE;
@@ -890,12 +923,11 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
     // the last step (or the first residual): every active subdomain was in it
     if (int rc = launch_factor(ctx, ctx->d_list, act, fac)) return rc;
     if (int rc = launch_solve(ctx, ctx->d_list, act, fac, ctx->R, -1.0, ctx->D, CLS_INNER_SOLVE)) return rc;
-    CK(cudaMemcpyAsync(ctx->h_bad, ctx->d_bad, I * sizeof(long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ctx->h_status, ctx->d_status, I * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     pend.clear();
     for (int i : act) {
-      const long long b = ctx->h_bad[i];
+      const long long b = ctx->res_bad[i];
       if (b >= 0) {
         char buf[160];
         snprintf(buf, sizeof buf, "%s@%lld", (b >> 32) ? "phi''(y)" : "phi'(y)", b & 0xffffffffLL);
@@ -916,8 +948,8 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
       if (int rc = upload_list(ctx, pend)) return rc;
       if (int rc = launch_residual(ctx, ctx->d_list, (int)pend.size(), x, ctx->V, ctx->D,
                                    ctx->d_alpha, eps, nullptr)) return rc;
-      CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      finish_residual(ctx, pend.data(), (int)pend.size(), false);
       next.clear();
       for (int i : pend) {
         const double trial = std::sqrt(ctx->h_norm2[i]);
@@ -947,8 +979,8 @@ static int sweep_impl(ocp_ctx* ctx, const double* x, double* fac, double eps_fac
       if (int rc = launch_residual(ctx, ctx->d_list, na, x, ctx->V, nullptr, nullptr, eps_next, ctx->R,
                                    true))
         return rc;
-      CK(cudaMemcpyAsync(ctx->h_norm2, ctx->d_norm2, I * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      finish_residual(ctx, acc.data(), na, true);
       for (int i : acc) {
         nrm[i] = std::sqrt(ctx->h_norm2[i]);
         iters[i] += 1;

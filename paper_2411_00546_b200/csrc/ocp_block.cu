@@ -73,6 +73,11 @@ void read_subt(long long* out, int n) {
 #define BPH_START() (void)0
 #define BPH_MARK(k) (void)0
 #endif
+#ifdef OCP_P1_SERIAL
+constexpr bool P1_SERIAL = true;
+#else
+constexpr bool P1_SERIAL = false;
+#endif
 constexpr int BF_JL_POINTS = 112;   // points per line whose diagonals fit the shared JL slot
 constexpr int BS_STAGES = 4;     // TMA ring depth of the solve
 #ifndef OCP_BS_PF_EARLY
@@ -552,7 +557,22 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           // (lookahead warps 0 and 4, one SM sub-partition, measured 13 % slower)
           const bool law = warp < LAW;
           const int lrank = warp, trank = warp - LAW;
+#ifdef OCP_P1_SERIAL
+          // A/B: no overlap - every warp does trailing tiles, then warps
+          // 0..LAW-1 invert the next pivot block with the FP64 pipe to themselves
+          for (int tI = warp; tI < total; tI += NW) tile(tI);
+          __syncthreads();
           if (law) {
+            pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad,
+                                 pivot_kmax(n, p0 + 32));
+          } else {
+            p3b(trank, NW - LAW);
+          }
+          __syncthreads();
+          if (false) {
+#else
+          if (law) {
+#endif
 #ifdef OCP_PHASE_TIMING
             const long long tla = clock64();
 #endif
@@ -564,7 +584,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
 #ifdef OCP_PHASE_TIMING
             if (tid == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tla));
 #endif
-          } else {
+          } else if (!P1_SERIAL) {
             for (int tI = trank; tI < total; tI += NW - LAW)
               if (tI != la0 && tI != la0 + 1) tile(tI);
             asm volatile("bar.sync 5, %0;" ::"n"(BF_THREADS) : "memory");

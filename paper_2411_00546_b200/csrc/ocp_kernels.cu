@@ -81,105 +81,102 @@ __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const dou
 // local residual (+ squared norm) of the listed subdomains at V + alpha_i D
 // _local_problem.local_residual (schwarz.py:181-186); R may be null (trial)
 // ---------------------------------------------------------------------------
-// A CTA owns RQ = 1024 consecutive local points q of one subdomain (flat
-// band order q = a * nc + b), 4 per thread.  The (v + alpha d) values of
-// q in [base - nc, base + RQ + nc) - the CTA's points plus one local row of
-// halo on either side - are staged in shared memory with contiguous,
-// coalesced loads (alpha d added once per element); the five stencil
-// entries of a point are then the staged values at q, q -+ 1, q -+ nc.
-// Every lane of a CTA but the last of a subdomain is busy (no 2D tile
-// padding), and the per-point index work is one division by nc.  f / y_d
-// are read at the point's global index (coalesced for orient 0, per-lane
-// strided rows for orient 1) before the staging barrier; the residual is
-// stored at q (coalesced).
-// With JD != null (the residual of an accepted step, or the first one) the
-// Jacobian diagonals of the same values and eps are produced as well - what
-// k_jacdiag would compute next - sharing x = -p/mu, the two square roots of
-// P_eps and phi'(y); *badkey receives this CTA's first nonfinite phi'/phi''
-// (k_jacdiag's packed key).  Every value is bitwise k_jacdiag's.
-template <int OR>
-__device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
-                                                const double* __restrict__ x,
-                                                const double2* __restrict__ V,
-                                                const double2* __restrict__ D, double al,
-                                                const double* __restrict__ f,
-                                                const double* __restrict__ yd, double eps,
-                                                double2* __restrict__ R, int base, double2* tv,
-                                                double2* __restrict__ JD,
-                                                unsigned long long& badkey) {
+// A CTA owns RQ consecutive local points q of one subdomain (flat band order
+// q = a * nc + b), RQ / RES_THREADS per thread in a ROLLED loop: one compact
+// code path for both orientations (the orientation only picks the offsets of
+// the four neighbours, taken in ascending global column order) - the
+// round-1 kernel unrolled the points and instantiated both orientations,
+// 10 k instructions, and lost 12 % of its issue slots to instruction fetch.
+//  * D == null (the first residual, the residual of an accepted step): the
+//    stencil reads V through L1 - no staging, no barrier; the loads of a
+//    point issue right where they are used.
+//  * D != null (line-search trial): v + alpha d (newton.py:106: product
+//    rounded first) of q in [base - nc, base + RQ + nc) - the CTA's points
+//    plus one local row of halo either side - is staged in shared memory
+//    once (contiguous, coalesced loads) and the stencil reads that.
+// f / y_d are read at the point's global index (coalesced for orient 0,
+// per-lane strided rows for orient 1); the residual is stored at q
+// (coalesced).  An absent stencil entry is fed as 0.0 instead of branching
+// (off * 0.0 = -0.0 and s + -0.0 == s bitwise), so the sums keep the
+// reference's CSR order and rounding.  The divisions and square roots of the
+// pointwise part are the branch-free div_fast / sqrt_fast / dvd_const_fast
+// (ocp_common.cuh; bitwise the IEEE intrinsics on their range); a point with
+// an operand outside the range is recomputed with the intrinsics.
+// With JD != null the Jacobian diagonals of the same values and eps are
+// produced as well - what k_jacdiag would compute next - sharing x = -p/mu,
+// the two square roots of P_eps and phi'(y); badkey receives the thread's
+// first nonfinite phi'/phi'' (k_jacdiag's packed key).  Every value is
+// bitwise k_jacdiag's.
+template <bool STAGED>
+__device__ __forceinline__ double residual_points(const SubInfo& s, const Phys& P,
+                                                  const double* __restrict__ x,
+                                                  const double2* __restrict__ V,
+                                                  const double* __restrict__ f,
+                                                  const double* __restrict__ yd, double eps,
+                                                  double2* __restrict__ R, int base,
+                                                  double2* __restrict__ JD,
+                                                  unsigned long long& badkey,
+                                                  const double2* __restrict__ D, double al,
+                                                  double2* tv) {
   constexpr int PPT = RQ / RES_THREADS;
   const int nr = s.nr, nc = s.nc, n = P.n, real = nr * nc;
   const long long Ntot = (long long)n * n;
+  const float inv_nc = 1.0f / (float)nc;
   const int lo = base - nc;
-  // 0. this thread's points: oriented coordinates, f / y_d loads in flight
-  int la[PPT], lb[PPT];
-  double fv[PPT], ydv[PPT];
-#pragma unroll
-  for (int u = 0; u < PPT; ++u) {
-    const int q = base + threadIdx.x + RES_THREADS * u;
-    la[u] = q / nc;
-    lb[u] = q - la[u] * nc;
-    fv[u] = ydv[u] = 0.0;
-    if (q < real) {
-      const long long g = OR == 0 ? (long long)(s.r0 + la[u]) * n + (s.c0 + lb[u])
-                                  : (long long)(s.r0 + lb[u]) * n + (s.c0 + la[u]);
-      fv[u] = f[g];
-      ydv[u] = yd[g];
-    }
-  }
-  // 1. stage v + alpha d (newton.py:106: product rounded first)
-  const int cnt = RQ + 2 * nc;
-  for (int e = threadIdx.x; e < cnt; e += RES_THREADS) {
-    const int q = lo + e;
-    double2 v = make_double2(0.0, 0.0);
-    if (q >= 0 && q < real) {
-      v = V[q];
-      if (D) {
+  if (STAGED) {
+    const int cnt = RQ + 2 * nc;
+    for (int e = threadIdx.x; e < cnt; e += RES_THREADS) {
+      const int q = lo + e;
+      double2 v = make_double2(0.0, 0.0);
+      if (q >= 0 && q < real) {
+        v = V[q];
         const double2 d = D[q];
         v.x = add(v.x, mul(al, d.x));
         v.y = add(v.y, mul(al, d.y));
       }
+      tv[e] = v;
     }
-    tv[e] = v;
+    __syncthreads();
   }
-  __syncthreads();
-  // 2. evaluate
+  const bool tr = s.orient != 0;
+  // neighbour offsets in ascending global column order (csr_matvec):
+  // (i-1,j), (i,j-1), (i,j+1), (i+1,j)
+  const int o0 = tr ? -1 : -nc, o1 = tr ? -nc : -1, o2 = tr ? nc : 1, o3 = tr ? 1 : nc;
   double acc = 0.0;
-#pragma unroll
+#ifndef OCP_RES_UNROLL
+#define OCP_RES_UNROLL 1
+#endif
+  constexpr int UNR = OCP_RES_UNROLL;   // rolled: measured fastest (instruction footprint)
+#pragma unroll UNR
   for (int u = 0; u < PPT; ++u) {
     const int q = base + threadIdx.x + RES_THREADS * u;
-    if (q >= real) continue;
-    const double2* c = tv + (q - lo);
+    if (q >= real) break;
+    // q / nc by a float reciprocal (off by at most one for q < 2^24) + fix-up
+    int a = __float2int_rz(__int2float_rn(q) * inv_nc), b = q - a * nc;
+    if (b < 0) { --a; b += nc; }
+    else if (b >= nc) { ++a; b -= nc; }
+    const int i = s.r0 + (tr ? b : a), j = s.c0 + (tr ? a : b);
+    const long long g0 = (long long)i * n + j;
+    const double fv = f[g0], ydv = yd[g0];
+    const double2* c = STAGED ? tv + (q - lo) : V + q;
     const double2 cv = c[0];
-    const bool in_u = la[u] > 0, in_d = la[u] < nr - 1, in_l = lb[u] > 0, in_r = lb[u] < nc - 1;
-    // the four neighbours in ascending global column order (csr_matvec):
-    // (i-1,j), (i,j-1), (i,j+1), (i+1,j)
-    double2 nv[4];
-    bool in[4];
-    if (OR == 0) {
-      nv[0] = c[-nc]; nv[1] = c[-1]; nv[2] = c[1]; nv[3] = c[nc];
-      in[0] = in_u; in[1] = in_l; in[2] = in_r; in[3] = in_d;
-    } else {
-      nv[0] = c[-1]; nv[1] = c[-nc]; nv[2] = c[nc]; nv[3] = c[1];
-      in[0] = in_l; in[1] = in_u; in[2] = in_d; in[3] = in_r;
-    }
-    // local part from the staged values, exterior part from the frozen
-    // global iterate; off * 0.0 = -0.0 and s + -0.0 == s bitwise for every s,
-    // so an absent entry contributes exactly nothing
+    const bool fu = a > 0, fd = a < nr - 1, fl = b > 0, fr = b < nc - 1;
+    const bool in0 = tr ? fl : fu, in1 = tr ? fu : fl, in2 = tr ? fd : fr, in3 = tr ? fr : fd;
+    const double2 zz = make_double2(0.0, 0.0);
+    // (an absent neighbour may lie outside the subdomain's vector: not loaded)
+    const double2 n0 = in0 ? c[o0] : zz, n1 = in1 ? c[o1] : zz, n2 = in2 ? c[o2] : zz, n3 = in3 ? c[o3] : zz;
+    // local part, exterior part from the frozen global iterate; off * 0.0 =
+    // -0.0 and s + -0.0 == s bitwise for every s, so an absent entry
+    // contributes exactly nothing
     double sly = 0.0, slp = 0.0;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (t == 2) {
-        sly = add(sly, mul(P.diag, cv.x));
-        slp = add(slp, mul(P.diag, cv.y));
-      }
-      sly = add(sly, mul(P.off, in[t] ? nv[t].x : 0.0));
-      slp = add(slp, mul(P.off, in[t] ? nv[t].y : 0.0));
-    }
+    sly = add(sly, mul(P.off, n0.x)); slp = add(slp, mul(P.off, n0.y));
+    sly = add(sly, mul(P.off, n1.x)); slp = add(slp, mul(P.off, n1.y));
+    sly = add(sly, mul(P.diag, cv.x)); slp = add(slp, mul(P.diag, cv.y));
+    sly = add(sly, mul(P.off, n2.x)); slp = add(slp, mul(P.off, n2.y));
+    sly = add(sly, mul(P.off, n3.x)); slp = add(slp, mul(P.off, n3.y));
     double sey = 0.0, sep = 0.0;
-    if (!(in[0] && in[1] && in[2] && in[3])) {
-      const int i = OR == 0 ? s.r0 + la[u] : s.r0 + lb[u];
-      const int j = OR == 0 ? s.c0 + lb[u] : s.c0 + la[u];
+    if (!(in0 && in1 && in2 && in3)) {
+      const bool in[4] = {in0, in1, in2, in3};
       const int di[4] = {-1, 0, 0, 1};
       const int dj[4] = {0, -1, 1, 0};
 #pragma unroll
@@ -194,12 +191,21 @@ __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
     const double ay = add(sly, sey), ap = add(slp, sep);
     const double y = cv.x, p = cv.y;
     // residual_rows (system.py:118-132) with the smoothed projection's parts kept
-    const double xm = dvd_const(-p, P.mu, P.rmu), a1 = add(xm, 1.0), b1 = sub(xm, 1.0);
-    const double sa = __dsqrt_rn(add(mul(a1, a1), eps)), sb = __dsqrt_rn(add(mul(b1, b1), eps));
+    bool slow = false;
+    double xm = dvd_const_fast(-p, P.mu, P.rmu, slow), a1 = add(xm, 1.0), b1 = sub(xm, 1.0);
+    double sa = sqrt_fast(add(mul(a1, a1), eps), slow), sb = sqrt_fast(add(mul(b1, b1), eps), slow);
     const double d1 = phi_d1(P, y);
-    const double ctrl = dvd_const(add(p, mul(P.mu, mul(0.5, sub(sa, sb)))), P.nu, P.rnu);
-    const double r1 = add(sub(add(ay, phi_value(P, y)), fv[u]), ctrl);
-    const double r2 = add(sub(add(ap, mul(d1, p)), y), ydv[u]);
+    double ctrl = dvd_const_fast(add(p, mul(P.mu, mul(0.5, sub(sa, sb)))), P.nu, P.rnu, slow);
+    double b12 = 0.0;
+    if (JD) b12 = dvd_const_fast(sub(1.0, mul(0.5, sub(div_fast(a1, sa, slow), div_fast(b1, sb, slow)))), P.nu, P.rnu, slow);
+    if (slow) {
+      xm = dvd_const(-p, P.mu, P.rmu), a1 = add(xm, 1.0), b1 = sub(xm, 1.0);
+      sa = __dsqrt_rn(add(mul(a1, a1), eps)), sb = __dsqrt_rn(add(mul(b1, b1), eps));
+      ctrl = dvd_const(add(p, mul(P.mu, mul(0.5, sub(sa, sb)))), P.nu, P.rnu);
+      if (JD) b12 = dvd_const(sub(1.0, mul(0.5, sub(dvd(a1, sa), dvd(b1, sb)))), P.nu, P.rnu);
+    }
+    const double r1 = add(sub(add(ay, phi_value(P, y)), fv), ctrl);
+    const double r2 = add(sub(add(ap, mul(d1, p)), y), ydv);
     acc = fma(r1, r1, acc);
     acc = fma(r2, r2, acc);
     if (R) R[q] = make_double2(r1, r2);
@@ -209,14 +215,10 @@ __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
       if (P.phi_kind == 0 && P.kappa != 0.0 && mul(P.kappa, y) > 700.0) bad1 = bad2 = true;
       if (P.phi_kind == 2 && y > 700.0) bad1 = bad2 = true;
       if (bad1 || bad2) {
-        const int i = OR == 0 ? s.r0 + la[u] : s.r0 + lb[u];
-        const int j = OR == 0 ? s.c0 + lb[u] : s.c0 + la[u];
         const unsigned long long ref = (unsigned long long)((i - s.r0) * (s.c1 - s.c0) + (j - s.c0));
         const unsigned long long key = ((bad1 ? 0ull : 1ull) << 32) | ref;
         badkey = key < badkey ? key : badkey;
       }
-      const double dp = mul(0.5, sub(dvd(a1, sa), dvd(b1, sb)));
-      const double b12 = dvd_const(sub(1.0, dp), P.nu, P.rnu);
       const double b21 = sub(mul(d2, p), 1.0);
       JD[2 * q] = make_double2(add(P.diag, d1), b12);
       JD[2 * q + 1] = make_double2(b21, 0.0);
@@ -227,17 +229,16 @@ __device__ __forceinline__ double residual_flat(const SubInfo& s, const Phys& P,
 
 size_t residual_smem_bytes(int max_nc) { return (size_t)(RQ + 2 * max_nc) * sizeof(double2); }
 
+template <bool DIRECT>
 __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const SubInfo* subs, const int* list, Phys P,
                                                       const double* x, const double* Vpool,
                                                       const double* Dpool, const double* alpha,
                                                       const double* f, const double* yd, double eps,
-                                                      double* Rpool, double* norm2, double* partials,
-                                                      unsigned int* counters, double* JDpool,
-                                                      unsigned long long* badparts, long long* bad) {
+                                                      double* Rpool, double* partials,
+                                                      double* JDpool, unsigned long long* badparts) {
   extern __shared__ double2 tv[];
   __shared__ double red[32];
   __shared__ unsigned long long bmin;
-  __shared__ bool is_last;
   const int sid = list ? list[blockIdx.x] : blockIdx.x;   // null list: all subdomains
   const SubInfo s = subs[sid];
   const double2* V = reinterpret_cast<const double2*>(Vpool + s.loc);
@@ -250,35 +251,25 @@ __global__ void __launch_bounds__(RES_THREADS, OCP_RES_MINB) k_residual(const Su
   double acc = 0.0;
   unsigned long long key = ~0ull;
   if (base < s.nr * s.nc) {
-    acc = s.orient == 0 ? residual_flat<0>(s, P, x, V, D, al, f, yd, eps, R, base, tv, JD, key)
-                        : residual_flat<1>(s, P, x, V, D, al, f, yd, eps, R, base, tv, JD, key);
+    acc = residual_points<!DIRECT>(s, P, x, V, f, yd, eps, R, base, JD, key, D, al, tv);
   }
   if (JD && key != ~0ull) atomicMin(&bmin, key);   // (bmin set before the staging barrier)
   const double tot = block_sum<RES_THREADS>(acc, red);
+  // one squared-norm partial (and first-bad key) per CTA; the host adds a
+  // subdomain's partials in CTA order after the copy it makes anyway, so a
+  // CTA ends without a fence / ticket round trip holding its SM slot
   if (threadIdx.x == 0) {
     partials[(long long)sid * gridDim.y + blockIdx.y] = tot;
     if (JD) badparts[(long long)sid * gridDim.y + blockIdx.y] = bmin;
-    __threadfence();
-    const unsigned int ticket = atomicAdd(&counters[sid], 1u);
-    is_last = (ticket == gridDim.y - 1);
-  }
-  __syncthreads();
-  if (is_last && threadIdx.x == 0) {
-    __threadfence();
-    double v = 0.0;
-    unsigned long long b = ~0ull;
-    for (int y = 0; y < (int)gridDim.y; ++y) {
-      v += partials[(long long)sid * gridDim.y + y];
-      if (JD) {
-        const unsigned long long by = badparts[(long long)sid * gridDim.y + y];
-        b = by < b ? by : b;
-      }
-    }
-    norm2[sid] = v;
-    if (JD) bad[sid] = b == ~0ull ? -1ll : (long long)b;
-    counters[sid] = 0u;
   }
 }
+
+template __global__ void k_residual<false>(const SubInfo*, const int*, Phys, const double*, const double*,
+                                           const double*, const double*, const double*, const double*,
+                                           double, double*, double*, double*, unsigned long long*);
+template __global__ void k_residual<true>(const SubInfo*, const int*, Phys, const double*, const double*,
+                                          const double*, const double*, const double*, const double*,
+                                          double, double*, double*, double*, unsigned long long*);
 
 // ---------------------------------------------------------------------------
 // Jacobian diagonals per point (system.py:135-144) + the reference's finite

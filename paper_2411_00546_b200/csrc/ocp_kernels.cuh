@@ -3,9 +3,9 @@
 #include "ocp_common.cuh"
 
 // local residual: RQ flat local points per CTA of RES_THREADS threads, min
-// resident CTAs per SM
+// resident CTAs per SM (measured on config 4 / 5: 128 x 4 x 8 fastest)
 #ifndef OCP_RES_THREADS
-#define OCP_RES_THREADS 256
+#define OCP_RES_THREADS 128
 #endif
 #ifndef OCP_RES_PPT
 #define OCP_RES_PPT 4
@@ -13,18 +13,18 @@
 constexpr int RES_THREADS = OCP_RES_THREADS;
 constexpr int RQ = OCP_RES_THREADS * OCP_RES_PPT;
 #ifndef OCP_RES_MINB
-#define OCP_RES_MINB 4
+#define OCP_RES_MINB 8
 #endif
 
 namespace ocp {
 
 __global__ void k_gather(const SubInfo* subs, const int* list, Phys P, const double* x, double* pool);
 size_t residual_smem_bytes(int max_nc);
+template <bool DIRECT>
 __global__ void k_residual(const SubInfo* subs, const int* list, Phys P, const double* x,
                            const double* Vpool, const double* Dpool, const double* alpha,
                            const double* f, const double* yd, double eps, double* Rpool,
-                           double* norm2, double* partials, unsigned int* counters,
-                           double* JDpool, unsigned long long* badparts, long long* bad);
+                           double* partials, double* JDpool, unsigned long long* badparts);
 __global__ void k_jacdiag(const SubInfo* subs, const int* list, Phys P, const double* Vpool,
                           double eps, double* JDpool, long long* bad);
 __global__ void k_update(const SubInfo* subs, const int* list, double* Vpool, const double* Dpool,

@@ -1,0 +1,103 @@
+// A/B of the 32x32 pivot inverse (P1 of k_block_factor): the shipped kernel
+// (pivot_inverse32 of ocp_block.cu, included here) on warps 0-3 of a 12-warp
+// CTA, alone and while warps 4-11 run DMMA trailing tiles on the same
+// shared-memory block - the situation inside the factor.  Prints cycles per
+// 2x2 pivot step.  Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a
+//   -I paper_2411_00546_b200/csrc -o tools/p1_ab tools/p1_ab.cu
+#include <cstdio>
+#define OCP_P1_AB 1
+#include "ocp_block.cu"
+
+using namespace ocp;
+
+__global__ void __launch_bounds__(384, 1)
+kern(int reps, int load, int variant, long long* out, double* dump) {
+  extern __shared__ __align__(16) double S[];
+  __shared__ int bad;
+  __shared__ volatile int done;
+  const int lds = 164;
+  double* W0 = S + 160 * lds;
+  double* W1 = W0 + 32 * WLD;
+  for (int e = threadIdx.x; e < 160 * lds; e += blockDim.x) {
+    const int i = e / lds, j = e % lds;
+    S[e] = (i == j) ? 4.0e6
+                    : ((i - j == 2 || j - i == 2) ? -1.0e6
+                                                  : 1e3 * ((i * 7 + j * 3) % 5 - 2) / (1 + (i - j) * (i - j)));
+  }
+  if (threadIdx.x == 0) { bad = 0; done = 0; }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  long long t0 = clock64();
+  if (warp < 4) {
+    for (int r = 0; r < reps; ++r) {
+      double* B = S + 32 * (r % 5) * lds + 32 * (r % 5);
+      if (variant == 0) pivot_inverse32<4>(B, lds, W0, W1, warp, lane, &bad, 32);
+      else pivot_inverse32_ref<4>(B, lds, W0, W1, warp, lane, &bad, 32);
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0) { out[blockIdx.x] = t1 - t0; done = 1; }
+  } else if (load) {
+    // trailing tiles on rows 32.. of a scratch copy region: same operand traffic
+    int r = 0;
+    while (!done) {
+      const int i0 = 32 * ((warp + r) % 4 + 1), j0 = 16 * ((warp * 3 + r) % 8 + 2);
+      double c[4][2][2];
+      load_c(S + i0 * lds + j0, lds, c, lane);
+      tile_32x16(S + i0 * lds, lds, S + j0, lds, c, lane, -1e-9);
+      store_c(S + i0 * lds + j0, lds, c, lane);
+      ++r;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) dump[blockIdx.x] = S[5] + bad;
+}
+
+// bitwise comparison of the two variants on the same block
+__global__ void __launch_bounds__(128, 1) kcmp(double* o0, double* o1) {
+  __shared__ double A[32 * 36], W0[32 * WLD], W1[32 * WLD];
+  __shared__ int bad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int v = 0; v < 2; ++v) {
+    for (int e = threadIdx.x; e < 32 * 36; e += 128) {
+      const int i = e / 36, j = e % 36;
+      // symmetric-in-the-P-sense test block: diagonally dominant with y<->p couplings
+      A[e] = (i == j) ? 4.0e6 + 1e3 * i
+                      : ((i ^ 1) == j ? 1.0e3 * (i + j)
+                                      : ((i - j == 2 || j - i == 2) ? -1.0e6 : 17.0 * ((i * 7 + j * 3) % 5 - 2)));
+    }
+    __syncthreads();
+    if (v == 0) pivot_inverse32<4>(A, 36, W0, W1, warp, lane, &bad, 32);
+    else pivot_inverse32_ref<4>(A, 36, W0, W1, warp, lane, &bad, 32);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * 32; e += 128) (v ? o1 : o0)[e] = A[(e >> 5) * 36 + (e & 31)];
+    __syncthreads();
+  }
+}
+
+int main() {
+  long long* d; double* dd; double *o0, *o1;
+  cudaMallocManaged(&d, 148 * 8); cudaMalloc(&dd, 148 * 8);
+  cudaMallocManaged(&o0, 1024 * 8); cudaMallocManaged(&o1, 1024 * 8);
+  kcmp<<<1, 128>>>(o0, o1);
+  cudaDeviceSynchronize();
+  int diff = 0;
+  for (int e = 0; e < 1024; ++e) diff += (o0[e] != o1[e]);
+  printf("bitwise: %d of 1024 entries differ (%s); sample %.17g %.17g\n", diff,
+         cudaGetErrorString(cudaGetLastError()), o0[33], o1[33]);
+  const int smem = (160 * 164 + 2 * 32 * WLD) * 8;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int variant = 0; variant < 2; ++variant)
+    for (int load = 0; load < 2; ++load) {
+      const int reps = 200;
+      for (int rep = 0; rep < 2; ++rep) {
+        kern<<<148, 384, smem>>>(reps, load, variant, d, dd);
+        cudaDeviceSynchronize();
+      }
+      double avg = 0;
+      for (int b = 0; b < 148; ++b) avg += (double)d[b] / 148;
+      printf("%s, %s: %.0f cycles per 32x32 inverse, %.1f per 2x2 step (%s)\n",
+             variant ? "reference (round-1 chain)" : "shipped", load ? "under DMMA load" : "alone",
+             avg / reps, avg / reps / 16, cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
