@@ -54,15 +54,16 @@ def build(force=False, verbose=False):
     return LIB
 
 
-TOOLS = {"fp64_peak": "fp64_peak.cu", "dmma_peak": "dmma_peak.cu"}
+TOOLS = {"fp64_peak": "fp64_peak.cu", "dmma_peak": "dmma_peak.cu", "rn_check": "rn_check.cu"}
 
 
 def build_tools(verbose=False):
-    """Peak probes used by bench.py for the FP64 roofline denominator."""
+    """Peak probes used by bench.py for the FP64 roofline denominator, and the
+    bitwise check of the branch-free division / square root (tests, -m gpu)."""
     tdir = os.path.join(os.path.dirname(HERE), "tools")
     for exe, src in TOOLS.items():
-        cmd = [nvcc(), "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-o",
-               os.path.join(tdir, exe), os.path.join(tdir, src)]
+        cmd = [nvcc(), "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-I", CSRC,
+               "-o", os.path.join(tdir, exe), os.path.join(tdir, src)]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

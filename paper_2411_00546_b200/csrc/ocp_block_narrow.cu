@@ -10,9 +10,21 @@
 // and nearly every line fits (ocp_abi.cu, bf_narrow).
 #include <cstring>
 
-#define OCP_BF_THREADS 192
-#define OCP_LAW 2
-#define OCP_BF_MINB 2
+#ifndef OCP_NW_THREADS
+#define OCP_NW_THREADS 192
+#endif
+#ifndef OCP_NW_LAW
+#define OCP_NW_LAW 2
+#endif
+#ifndef OCP_NW_MINB
+#define OCP_NW_MINB 2
+#endif
+#ifdef OCP_NW_SERIAL
+#define OCP_P1_SERIAL 1
+#endif
+#define OCP_BF_THREADS OCP_NW_THREADS
+#define OCP_LAW OCP_NW_LAW
+#define OCP_BF_MINB OCP_NW_MINB
 #define OCP_BF_SMEM_MAX_NPB 96
 #define OCP_NARROW_INSTANCE 1
 #define ocp ocp_nw

@@ -574,3 +574,19 @@ def test_tiny_grids_residual_and_jvp_match_oracle(n, s1, s2, m):
     d = rng.standard_normal(x.shape[0])
     out = raspen_jacobian_apply(x, d, dec, spec, 1e-2, corr)
     assert rel_l2(out, O.raspen_jvp(prob, x, d, 1e-2, co)) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_branch_free_division_and_sqrt_are_bitwise_ieee():
+    """div_fast / sqrt_fast / dvd_const_fast of the local residual (ocp_common.cuh) against
+    __ddiv_rn / __dsqrt_rn: random, near-tie and residual-shaped operands, 4e9 comparisons
+    (tools/rn_check.cu; exit code 1 on any mismatch)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "rn_check")
+    if not os.path.exists(exe):
+        from paper_2411_00546_b200._build import build_tools
+        build_tools()
+    out = subprocess.run([exe, "1024"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "mismatches div 0, sqrt 0, dvd_const 0, near-tie 0" in out.stdout, out.stdout
