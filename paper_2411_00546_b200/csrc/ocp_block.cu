@@ -150,6 +150,9 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   }
   asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   bool ok = true;
+#ifdef OCP_PHASE_TIMING
+  const long long t_piv = clock64();
+#endif
 #pragma unroll 1
   for (int k = 0; k < kmax; k += 2) {
     const double* Wr = (k & 2) ? W1 : W0;
@@ -185,6 +188,9 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
     }
     asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   }
+#ifdef OCP_PHASE_TIMING
+  if (P1_SERIAL && wsub == 0 && lane == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - t_piv));
+#endif
 #pragma unroll
   for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
   if (!ok) *bad = 1;
@@ -562,6 +568,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           // 0..LAW-1 invert the next pivot block with the FP64 pipe to themselves
           for (int tI = warp; tI < total; tI += NW) tile(tI);
           __syncthreads();
+          BPH_MARK(3);
           if (law) {
             pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad,
                                  pivot_kmax(n, p0 + 32));
@@ -569,6 +576,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
             p3b(trank, NW - LAW);
           }
           __syncthreads();
+          BPH_MARK(5);
           if (false) {
 #else
           if (law) {

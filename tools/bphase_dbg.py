@@ -11,10 +11,11 @@ import os
 lib = ctypes.CDLL(os.environ.get("OCP_LIB", "paper_2411_00546_b200/libocpgpu.so"))
 buf = (ctypes.c_ulonglong * 16)()
 lib.ocp_debug_phase(buf)
-v = np.array(list(buf), dtype=float)[8:]
+v = np.array(list(buf), dtype=float)[8:] / 2.0   # the counters cover the warm-up launch and the timed one
 names = ["", "E2", "P2 row block", "P3a trailing", "P3b column block", "P1 pivot inverse",
          "store (TMA issue + wait read)", "E1 scale"]
 tot = v[1:8].sum()
+print(f"per launch, summed over the CTAs (cycles); with -DOCP_P1_SERIAL slot 0 is the pivot-step loop alone")
 print(f"lookahead path (tile + pivot inverse, inside P3a): {v[0]:.3e} cycles")
 
 for k in range(1, 8):

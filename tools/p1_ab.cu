@@ -31,13 +31,91 @@ kern(int reps, int load, int variant, long long* out, double* dump) {
   if (warp < 4) {
     for (int r = 0; r < reps; ++r) {
       double* B = S + 32 * (r % 5) * lds + 32 * (r % 5);
-      if (variant == 0) pivot_inverse32<4>(B, lds, W0, W1, warp, lane, &bad, 32);
-      else pivot_inverse32_ref<4>(B, lds, W0, W1, warp, lane, &bad, 32);
+      pivot_inverse32<4>(B, lds, W0, W1, warp, lane, &bad, 32);
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) { out[blockIdx.x] = t1 - t0; done = 1; }
   } else if (load) {
     // trailing tiles on rows 32.. of a scratch copy region: same operand traffic
+    int r = 0;
+    while (!done) {
+      const int i0 = 32 * ((warp + r) % 4 + 1), j0 = 16 * ((warp * 3 + r) % 8 + 2);
+      double c[4][2][2];
+      load_c(S + i0 * lds + j0, lds, c, lane);
+      tile_32x16(S + i0 * lds, lds, S + j0, lds, c, lane, -1e-9);
+      store_c(S + i0 * lds + j0, lds, c, lane);
+      ++r;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) dump[blockIdx.x] = S[5] + bad;
+}
+
+// the factor's serial schedule: every warp does trailing tiles, barrier, then
+// warps 0-3 invert a pivot block while the others wait at the next barrier;
+// only the inverse is timed (clock64 around the call on thread 0)
+__global__ void __launch_bounds__(384, 1)
+kern_serial(int reps, int tiles_per_warp, long long* out, double* dump) {
+  extern __shared__ __align__(16) double S[];
+  __shared__ int bad;
+  const int lds = 164;
+  double* W0 = S + 160 * lds;
+  double* W1 = W0 + 32 * WLD;
+  for (int e = threadIdx.x; e < 160 * lds; e += blockDim.x) {
+    const int i = e / lds, j = e % lds;
+    S[e] = (i == j) ? 4.0e6
+                    : ((i - j == 2 || j - i == 2) ? -1.0e6
+                                                  : 1e3 * ((i * 7 + j * 3) % 5 - 2) / (1 + (i - j) * (i - j)));
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  long long tot = 0;
+  for (int r = 0; r < reps; ++r) {
+    for (int t = 0; t < tiles_per_warp; ++t) {
+      const int i0 = 32 * ((warp + r + t) % 4 + 1), j0 = 16 * ((warp * 3 + r + t) % 8 + 2);
+      double c[4][2][2];
+      load_c(S + i0 * lds + j0, lds, c, lane);
+      tile_32x16(S + i0 * lds, lds, S + j0, lds, c, lane, -1e-9);
+      store_c(S + i0 * lds + j0, lds, c, lane);
+    }
+    __syncthreads();
+    const long long t0 = clock64();
+    if (warp < 4) pivot_inverse32<4>(S, lds, W0, W1, warp, lane, &bad, 32);
+    if (threadIdx.x == 0) tot += clock64() - t0;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { out[blockIdx.x] = tot; dump[blockIdx.x] = S[5] + bad; }
+}
+
+// sub-partition isolation: the inverse on PW warps that all sit on SM
+// sub-partition 0 (warp ids 0, 4, 8, 12: warp % 4 == 0) while the warps of the
+// other three sub-partitions run DMMA tiles; the remaining warps of
+// sub-partition 0 idle
+template <int PW>
+__global__ void __launch_bounds__(512, 1)
+kern_iso(int reps, int load, long long* out, double* dump) {
+  extern __shared__ __align__(16) double S[];
+  __shared__ int bad;
+  __shared__ volatile int done;
+  const int lds = 164;
+  double* W0 = S + 160 * lds;
+  double* W1 = W0 + 32 * WLD;
+  for (int e = threadIdx.x; e < 160 * lds; e += blockDim.x) {
+    const int i = e / lds, j = e % lds;
+    S[e] = (i == j) ? 4.0e6
+                    : ((i - j == 2 || j - i == 2) ? -1.0e6
+                                                  : 1e3 * ((i * 7 + j * 3) % 5 - 2) / (1 + (i - j) * (i - j)));
+  }
+  if (threadIdx.x == 0) { bad = 0; done = 0; }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t0 = clock64();
+  if ((warp & 3) == 0 && (warp >> 2) < PW) {
+    for (int r = 0; r < reps; ++r)
+      pivot_inverse32<PW>(S + 32 * (r % 5) * lds + 32 * (r % 5), lds, W0, W1, warp >> 2, lane, &bad, 32);
+    if (threadIdx.x == 0) { out[blockIdx.x] = clock64() - t0; done = 1; }
+  } else if (load && (warp & 3) != 0 && warp < 12) {
     int r = 0;
     while (!done) {
       const int i0 = 32 * ((warp + r) % 4 + 1), j0 = 16 * ((warp * 3 + r) % 8 + 2);
@@ -66,8 +144,7 @@ __global__ void __launch_bounds__(128, 1) kcmp(double* o0, double* o1) {
                                       : ((i - j == 2 || j - i == 2) ? -1.0e6 : 17.0 * ((i * 7 + j * 3) % 5 - 2)));
     }
     __syncthreads();
-    if (v == 0) pivot_inverse32<4>(A, 36, W0, W1, warp, lane, &bad, 32);
-    else pivot_inverse32_ref<4>(A, 36, W0, W1, warp, lane, &bad, 32);
+    pivot_inverse32<4>(A, 36, W0, W1, warp, lane, &bad, 32);
     __syncthreads();
     for (int e = threadIdx.x; e < 32 * 32; e += 128) (v ? o1 : o0)[e] = A[(e >> 5) * 36 + (e & 31)];
     __syncthreads();
@@ -99,5 +176,34 @@ int main() {
              variant ? "reference (round-1 chain)" : "shipped", load ? "under DMMA load" : "alone",
              avg / reps, avg / reps / 16, cudaGetErrorString(cudaGetLastError()));
     }
+  auto iso = [&](auto kfn, int pw, int threads) {
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int load = 0; load < 2; ++load) {
+      const int reps = 200;
+      for (int rep = 0; rep < 2; ++rep) {
+        kfn<<<148, threads, smem>>>(reps, load, d, dd);
+        cudaDeviceSynchronize();
+      }
+      double avg = 0;
+      for (int b = 0; b < 148; ++b) avg += (double)d[b] / 148;
+      printf("inverse on %d warps of sub-partition 0, %s: %.0f cycles per 32x32 inverse, %.1f per 2x2 step (%s)\n",
+             pw, load ? "DMMA tiles on the 9 warps of sub-partitions 1-3" : "alone", avg / reps,
+             avg / reps / 16, cudaGetErrorString(cudaGetLastError()));
+    }
+  };
+  iso(kern_iso<2>, 2, 384);
+  iso(kern_iso<4>, 4, 512);
+  cudaFuncSetAttribute(kern_serial, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  for (int tpw : {0, 1, 2, 4}) {
+    const int reps = 100;
+    for (int rep = 0; rep < 2; ++rep) {
+      kern_serial<<<148, 384, smem>>>(reps, tpw, d, dd);
+      cudaDeviceSynchronize();
+    }
+    double avg = 0;
+    for (int b = 0; b < 148; ++b) avg += (double)d[b] / 148;
+    printf("serial schedule, %d tiles per warp before each inverse: %.0f cycles per 32x32 inverse (%s)\n",
+           tpw, avg / reps, cudaGetErrorString(cudaGetLastError()));
+  }
   return 0;
 }
