@@ -129,6 +129,13 @@ int ocp_local_residual(ocp_ctx* ctx, const double* x_dev, const double* v_ref_de
                        double eps, double* r_ref_dev);
 int ocp_local_direction(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
                         double eps, double* d_ref_dev);
+/* Squared norms of the line-search trial residual ||F_i(v_i + alpha_i d_i)||^2 of every
+ * subdomain (newton.py:96-112: residual(x + alpha * d), product rounded first), the
+ * staged-direction instance of the residual kernel; v, d in the reference layout,
+ * alpha_host / norm2_host: I doubles on the host.  Parity hook. */
+int ocp_local_residual_trial(ocp_ctx* ctx, const double* x_dev, const double* v_ref_dev,
+                             const double* d_ref_dev, const double* alpha_host, double eps,
+                             double* norm2_host);
 
 /* ---- GMRES vector kernels (krylov.py:44-151), deterministic reductions -- */
 int ocp_vec_nrm2(ocp_ctx* ctx, long long n, const double* x, double* out_host);

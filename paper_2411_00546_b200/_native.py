@@ -52,6 +52,7 @@ SIGNATURES = {
     "ocp_raspen_jvp": [_vp, _vp, _vp, _vp],
     "ocp_local_values": [_vp, _vp],
     "ocp_local_residual": [_vp, _vp, _vp, _d, _vp],
+    "ocp_local_residual_trial": [_vp, _vp, _vp, _vp, _vp, _d, _vp],
     "ocp_local_direction": [_vp, _vp, _vp, _d, _vp],
     "ocp_vec_nrm2": [_vp, _ll, _vp, _c_dbl_p],
     "ocp_vec_dot": [_vp, _ll, _vp, _vp, _c_dbl_p],

@@ -1084,6 +1084,26 @@ int ocp_local_residual(ocp_ctx* ctx, const double* x, const double* v_ref, doubl
   return OCP_OK;
 }
 
+int ocp_local_residual_trial(ocp_ctx* ctx, const double* x, const double* v_ref, const double* d_ref,
+                             const double* alpha_host, double eps, double* norm2_host) {
+  if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
+  if (!alpha_host || !norm2_host) return fail(ctx, OCP_ERR_ARG, "null argument");
+  cudaStream_t st = ctx->stream;
+  const int I = ctx->I;
+  k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, v_ref, ctx->B);
+  CKL();
+  k_ref_to_band<<<I, 256, 0, st>>>(ctx->d_subs, d_ref, ctx->D);
+  CKL();
+  for (int i = 0; i < I; ++i) ctx->h_alpha[i] = alpha_host[i];
+  CK(cudaMemcpyAsync(ctx->d_alpha, ctx->h_alpha, I * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (int rc = launch_residual(ctx, ctx->d_list_all, I, x, ctx->B, ctx->D, ctx->d_alpha, eps, nullptr))
+    return rc;
+  CK(cudaStreamSynchronize(st));
+  finish_residual(ctx, nullptr, I, false);
+  for (int i = 0; i < I; ++i) norm2_host[i] = ctx->h_norm2[i];
+  return OCP_OK;
+}
+
 int ocp_local_direction(ocp_ctx* ctx, const double* x, const double* v_ref, double eps, double* d_ref) {
   if (ctx && ctx->I == 0) return fail(ctx, OCP_ERR_ARG, "grid-only context has no subdomains");
   cudaStream_t st = ctx->stream;

@@ -88,6 +88,49 @@ def test_local_residual_multi_chunk_bitwise(n, s1, s2, m):
     np.testing.assert_array_equal(rd.to_host(), ref)
 
 
+@pytest.mark.parametrize("n,s1,s2,m", [(127, 2, 3, 4), (63, 1, 1, 0), (40, 3, 2, 5)])
+def test_trial_residual_norms_bitwise(n, s1, s2, m):
+    """The line-search trial ||F_i(v_i + alpha_i d_i)||^2 (newton.py:96-112) through the
+    staged-direction instance of the residual kernel: v + alpha * d with the product
+    rounded first, the frozen-exterior local residual of the oracle (schwarz.py:174-186)
+    bitwise for the cubic phi, and the squared norm within the summation-order bound
+    (per-thread / per-CTA partial sums instead of numpy's pairwise sum)."""
+    import ctypes
+    phi, nu, mu, eps = make_phi("cubic"), 1e-3, 1e-2, 1e-3
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, s1, s2, m)
+    eng = build_local_systems(dec, spec)
+    prob = O.Problem(n, s1, s2, m, phi, nu, mu, spec.f, spec.y_d)
+    rng = np.random.default_rng(11 + n)
+    x = 0.3 * rng.standard_normal(2 * n * n)
+    v = np.concatenate([x[s.pair_idx] + 0.01 for s in dec.subdomains])
+    d = 0.1 * rng.standard_normal(v.shape[0])
+    I = len(dec.subdomains)
+    alpha = 0.5 ** rng.integers(0, 4, I).astype(float)
+    offs = np.cumsum([0] + [2 * s.size for s in dec.subdomains])
+    xd, vd, dd = eng.from_host(x), eng.from_host(v), eng.from_host(d)
+    out = (ctypes.c_double * I)()
+    al = (ctypes.c_double * I)(*alpha)
+    eng.check(eng.lib.ocp_local_residual_trial(eng.ctx, xd.ptr, vd.ptr, dd.ptr, al, eps, out), "trial")
+    # the same values staged with alpha = 0 give bitwise the same squared norms
+    out0 = (ctypes.c_double * I)()
+    zero = (ctypes.c_double * I)(*([0.0] * I))
+    vt_dev = eng.from_host(np.concatenate([v[offs[i]:offs[i + 1]] + alpha[i] * d[offs[i]:offs[i + 1]]
+                                           for i in range(I)]))
+    eng.check(eng.lib.ocp_local_residual_trial(eng.ctx, xd.ptr, vt_dev.ptr, dd.ptr, zero, eps, out0), "trial0")
+    assert list(out) == list(out0)
+    # the staged values feed the same stencil: the residual AT v + alpha d is bitwise the oracle's
+    vt = np.concatenate([v[offs[i]:offs[i + 1]] + alpha[i] * d[offs[i]:offs[i + 1]] for i in range(I)])
+    rd = eng.vector(v.shape[0])
+    eng.check(eng.lib.ocp_local_residual(eng.ctx, xd.ptr, eng.from_host(vt).ptr, eps, rd.ptr), "res")
+    r = rd.to_host()
+    for i in range(I):
+        ref = prob.local_fns(i, x)[0](vt[offs[i]:offs[i + 1]], eps)
+        np.testing.assert_array_equal(r[offs[i]:offs[i + 1]], ref)
+        want = float(np.dot(ref, ref))
+        assert abs(out[i] - want) <= 1e-13 * want, (i, out[i], want)
+
+
 @pytest.mark.parametrize("case", UNIT_CASES, ids=IDS)
 def test_local_direction_matches_superlu(case):
     import scipy.sparse.linalg as spla
