@@ -23,6 +23,7 @@
 #include "ocp_kernels.cuh"
 
 using namespace ocp;
+namespace ocp_nw { void read_bphase(unsigned long long* out); }
 namespace ocp { void read_bphase(unsigned long long* out);
                 void read_aphase(unsigned long long* out); void read_subt(long long* out, int n); }
 
@@ -1696,6 +1697,11 @@ int ocp_debug_subt(long long* out, int n) {
 int ocp_debug_phase(unsigned long long* out) {
   for (int i = 0; i < 8; ++i) out[i] = 0;   // (slots of the removed band format)
   ocp::read_bphase(out + 8);
+  {   // + the narrow-line instance's counters (one of the two instances runs per context)
+    unsigned long long nw[8];
+    ocp_nw::read_bphase(nw);
+    for (int i = 0; i < 8; ++i) out[8 + i] += nw[i];
+  }
   ocp::read_aphase(out + 16);
   return 0;
 }
