@@ -11,7 +11,7 @@
 using namespace ocp;
 
 __global__ void __launch_bounds__(384, 1)
-kern(int reps, int load, int variant, long long* out, double* dump) {
+kern(int reps, int load, int variant, long long* out, double* dump, unsigned long long* tiles = nullptr) {
   extern __shared__ __align__(16) double S[];
   __shared__ int bad;
   __shared__ volatile int done;
@@ -35,7 +35,7 @@ kern(int reps, int load, int variant, long long* out, double* dump) {
     }
     long long t1 = clock64();
     if (threadIdx.x == 0) { out[blockIdx.x] = t1 - t0; done = 1; }
-  } else if (load) {
+  } else if (warp < 4 + load) {
     // trailing tiles on rows 32.. of a scratch copy region: same operand traffic
     int r = 0;
     while (!done) {
@@ -46,6 +46,7 @@ kern(int reps, int load, int variant, long long* out, double* dump) {
       store_c(S + i0 * lds + j0, lds, c, lane);
       ++r;
     }
+    if (tiles && lane == 0) atomicAdd(tiles, (unsigned long long)r);
   }
   __syncthreads();
   if (threadIdx.x == 0) dump[blockIdx.x] = S[5] + bad;
@@ -163,19 +164,23 @@ int main() {
          cudaGetErrorString(cudaGetLastError()), o0[33], o1[33]);
   const int smem = (160 * 164 + 2 * 32 * WLD) * 8;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int variant = 0; variant < 2; ++variant)
-    for (int load = 0; load < 2; ++load) {
-      const int reps = 200;
-      for (int rep = 0; rep < 2; ++rep) {
-        kern<<<148, 384, smem>>>(reps, load, variant, d, dd);
-        cudaDeviceSynchronize();
-      }
-      double avg = 0;
-      for (int b = 0; b < 148; ++b) avg += (double)d[b] / 148;
-      printf("%s, %s: %.0f cycles per 32x32 inverse, %.1f per 2x2 step (%s)\n",
-             variant ? "reference (round-1 chain)" : "shipped", load ? "under DMMA load" : "alone",
-             avg / reps, avg / reps / 16, cudaGetErrorString(cudaGetLastError()));
+  unsigned long long* tiles;
+  cudaMallocManaged(&tiles, 8);
+  for (int load : {0, 4, 8}) {
+    const int reps = 200;
+    for (int rep = 0; rep < 2; ++rep) {
+      *tiles = 0;
+      kern<<<148, 384, smem>>>(reps, load, 0, d, dd, tiles);
+      cudaDeviceSynchronize();
     }
+    double avg = 0;
+    for (int b = 0; b < 148; ++b) avg += (double)d[b] / 148;
+    // tile rate: 32x16x32 tiles per 1000 cycles and SM while the inverses run
+    printf("inverse on warps 0-3, %d warps on DMMA tiles: %.0f cycles per 32x32 inverse, %.1f per 2x2 step; "
+           "%.2f tiles per 1000 cycles and SM (%s)\n",
+           load, avg / reps, avg / reps / 16, 1000.0 * (double)*tiles / 148 / avg,
+           cudaGetErrorString(cudaGetLastError()));
+  }
   auto iso = [&](auto kfn, int pw, int threads) {
     cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     for (int load = 0; load < 2; ++load) {
