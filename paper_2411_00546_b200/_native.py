@@ -103,6 +103,8 @@ _lock = threading.Lock()
 def load(path=LIB_PATH):
     """Load and type the library (does not touch the GPU)."""
     global _lib
+    if _lib is not None:   # (no lock on the hot path: load() is also reached from finalizers)
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib
@@ -174,32 +176,62 @@ class BufferPool:
 
 class _RetiredCache:
     """Buffers of destroyed engines (their streams are idle), reused by size
-    across engines like a caching allocator; bounded, thread-safe."""
+    across engines like a caching allocator; bounded, thread-safe.
+
+    ``give`` runs from garbage-collection finalizers (``Engine`` teardown,
+    ``DeviceBuffer.__del__``), and a collection can start at any allocation -
+    also inside ``take`` / ``give`` while this thread holds the lock.  So
+    ``give`` never blocks on the lock: when it is taken the buffer is parked
+    in ``_pending`` (list.append is atomic) and filed by the next caller that
+    holds the lock.  (A blocking acquire here deadlocked the thread against
+    itself: a flaky hang of the GPU test suite.)
+    """
 
     def __init__(self, limit_bytes=16 << 30):
         self.free = {}
         self.cached = 0
         self.limit = limit_bytes
         self.lock = threading.Lock()
+        self._pending = []
 
-    def take(self, nbytes):
-        with self.lock:
-            lst = self.free.get(nbytes)
-            if lst:
-                self.cached -= nbytes
-                return lst.pop()
-        return None
-
-    def give(self, addr, nbytes):
-        with self.lock:
+    def _file_locked(self):
+        """File the parked buffers (lock held); returns those over the limit."""
+        over = []
+        while self._pending:
+            addr, nbytes = self._pending.pop()
             if self.cached + nbytes <= self.limit:
                 self.free.setdefault(nbytes, []).append(addr)
                 self.cached += nbytes
-                return
-        _raw_free(addr)
+            else:
+                over.append(addr)
+        return over
+
+    def take(self, nbytes):
+        addr = None
+        with self.lock:
+            over = self._file_locked()
+            lst = self.free.get(nbytes)
+            if lst:
+                addr = lst.pop()
+                self.cached -= nbytes
+        for a in over:
+            _raw_free(a)
+        return addr
+
+    def give(self, addr, nbytes):
+        self._pending.append((addr, nbytes))
+        if not self.lock.acquire(blocking=False):
+            return   # the holder (possibly this thread, below us on the stack) files it later
+        try:
+            over = self._file_locked()
+        finally:
+            self.lock.release()
+        for a in over:
+            _raw_free(a)
 
     def empty(self):
         with self.lock:
+            self._file_locked()
             lists, self.free, self.cached = list(self.free.values()), {}, 0
         for lst in lists:
             for addr in lst:

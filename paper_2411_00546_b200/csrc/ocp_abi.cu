@@ -623,10 +623,12 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   const size_t pbytes = ctx->pool_len * sizeof(double);
   for (double** p : {&ctx->V, &ctx->R, &ctx->D, &ctx->B}) {
     CKC(gmalloc(p, pbytes));
-    CKC(cudaMemset(*p, 0, pbytes));
+    // (on the context's stream: it is non-blocking, so a legacy-default-stream
+    // memset would not be ordered before the first kernels that use the buffer)
+    CKC(cudaMemsetAsync(*p, 0, pbytes, ctx->stream));
   }
   CKC(gmalloc(&ctx->JD, 2 * pbytes));
-  CKC(cudaMemset(ctx->JD, 0, 2 * pbytes));
+  CKC(cudaMemsetAsync(ctx->JD, 0, 2 * pbytes, ctx->stream));
   CKC(gmalloc(&ctx->d_list_all, I * sizeof(int)));
   CKC(gmalloc(&ctx->d_list, I * sizeof(int)));
   CKC(gmalloc(&ctx->d_status, I * sizeof(int)));
@@ -676,9 +678,21 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   // are enough subdomains to fill them and nearly every line fits its
   // 96-unknown shared-memory block (ocp_block_narrow.cu)
   if (I >= 2 * ctx->num_sms) {
+    // (an instance whose block size is an odd multiple of 16 factors lines padded
+    // to 16 with a half-width last panel: such lines get pad_ = NPS)
+    const int nmax = narrow_factor_max_npb();
+    const bool half = (nmax & 16) != 0;
     int fit = 0;
-    for (auto& sub : ctx->subs) fit += sub.pad_ <= narrow_factor_max_npb();
+    for (auto& sub : ctx->subs) fit += (half ? sub.NPS : sub.pad_) <= nmax;
     ctx->bf_narrow = 10LL * fit >= 9LL * I;
+    if (ctx->bf_narrow && half) {
+      ctx->maxNPB = 0;
+      for (auto& sub : ctx->subs) {
+        if (sub.NPS <= nmax && (sub.NPS & 16) && sub.NPS >= 48) sub.pad_ = sub.NPS;
+        ctx->maxNPB = std::max(ctx->maxNPB, sub.pad_);
+      }
+      CKC(cudaMemcpy(ctx->d_subs, ctx->subs.data(), I * sizeof(SubInfo), cudaMemcpyHostToDevice));
+    }
   }
   const int bf_per_sm = ctx->bf_narrow ? narrow_factor_ctas_per_sm() : 1;
   const int bf_max_npb = ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB;
@@ -715,10 +729,10 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   }
   CKC(gmalloc(&ctx->red_partials, RED_BLOCKS * sizeof(double)));
   CKC(gmalloc(&ctx->red_counter, sizeof(unsigned int)));
-  CKC(cudaMemset(ctx->red_counter, 0, sizeof(unsigned int)));
+  CKC(cudaMemsetAsync(ctx->red_counter, 0, sizeof(unsigned int), ctx->stream));
   CKC(gmalloc(&ctx->arn_bar, sizeof(unsigned long long)));
   CKC(gmalloc(&ctx->arn_partials, 2 * 2048 * sizeof(double)));
-  CKC(cudaMemset(ctx->arn_bar, 0, sizeof(unsigned long long)));
+  CKC(cudaMemsetAsync(ctx->arn_bar, 0, sizeof(unsigned long long), ctx->stream));
   CKC(gmalloc(&ctx->d_result, 8 * sizeof(double)));
   ctx->h_cap = 4096;
   CKC(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));

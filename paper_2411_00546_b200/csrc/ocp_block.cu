@@ -134,9 +134,12 @@ constexpr int LAW = OCP_LAW;   // lookahead warps (0 .. LAW-1): the next pivot i
 // line's n unknowns (decoupled: zero rows / columns outside the diagonal), so
 // their Gauss-Jordan steps are exact no-ops and are skipped - the last panel
 // of a 72-unknown line (NPB 96) takes 4 steps instead of 16.
+// bw: rows / columns of the block that exist in storage (32, or 16 for the
+// half-width last panel of a line padded to 16: the rest is identity, held
+// in registers only).
 template <int PW>
 __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, double* W1, int wsub,
-                                             int lane, int* bad, int kmax) {
+                                             int lane, int* bad, int kmax, int bw = 32) {
   // Gauss-Jordan with 2x2 pivot blocks: 16 dependent steps instead of 32.
   // Step s eliminates rows/columns K = {k, k+1}, k = 2s:
   //   S[K,K] <- P^{-1};  S[K,j] <- P^{-1} S[K,j];  S[i,K] <- -S[i,K] P^{-1};
@@ -145,8 +148,9 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   double c[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    c[i] = B[(R * wsub + i) * lds + lane];
-    W0[(R * wsub + i) * WLD + lane] = c[i];
+    const int row = R * wsub + i;
+    c[i] = (row < bw && lane < bw) ? B[row * lds + lane] : (row == lane ? 1.0 : 0.0);
+    W0[row * WLD + lane] = c[i];
   }
   asm volatile("bar.sync 2, %0;" ::"n"(32 * PW) : "memory");
   bool ok = true;
@@ -192,7 +196,8 @@ __device__ __noinline__ void pivot_inverse32(double* B, int lds, double* W0, dou
   if (P1_SERIAL && wsub == 0 && lane == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - t_piv));
 #endif
 #pragma unroll
-  for (int i = 0; i < R; ++i) B[(R * wsub + i) * lds + lane] = c[i];
+  for (int i = 0; i < R; ++i)
+    if (R * wsub + i < bw && lane < bw) B[(R * wsub + i) * lds + lane] = c[i];
   if (!ok) *bad = 1;
 }
 // real pivots of the 32x32 pivot block at p0 (n even: 2x2 pivot pairs stay whole)
@@ -201,21 +206,28 @@ __device__ __forceinline__ int pivot_kmax(int n, int p0) {
   return k < 32 ? (k > 0 ? k : 0) : 32;
 }
 
+// one DMMA tile of 8 MI rows x 16 columns over KK pivot columns:
+//   C (+)= sgn * A[8 MI x KK] * B[KK x 16]
+//   A element (m, k) at A + m*lda + k ; B element (k, n) at B + k*ldb + n
+// (MI, KK) = (4, 32) everywhere except the half-width last panel of a line
+// padded to 16 (narrow lines: 72 unknowns at NPB = 80), where the row tile
+// has 16 rows (MI = 2) and / or the pivot panel 16 columns (KK = 16).
 #ifdef OCP_DFMA_ONLY
 // A/B build (tools/build_variant.py dfma -DOCP_DFMA_ONLY): the same tiles,
 // register layout and shared-memory operands, multiplied with DFMA instead of
-// DMMA - each lane accumulates its 16 (tile) / 16 (strip) outputs from one
-// A element per row and double2 B loads per k.  Justifies the DMMA choice
-// with a measurement (profiles/r2_dmma_vs_dfma.md).
-__device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
-                                           double c[4][2][2], int lane, double sgn) {
+// DMMA - each lane accumulates its outputs from one A element per row and
+// double2 B loads per k.  Justifies the DMMA choice with a measurement
+// (profiles/r2_dmma_vs_dfma.md).
+template <int MI, int KK>
+__device__ __forceinline__ void tile_mk(const double* A, int lda, const double* B, int ldb,
+                                        double c[4][2][2], int lane, double sgn) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll 4
-  for (int k = 0; k < 32; ++k) {
+  for (int k = 0; k < KK; ++k) {
     const double2 b0 = *reinterpret_cast<const double2*>(B + k * ldb + 2 * t4);
     const double2 b1 = *reinterpret_cast<const double2*>(B + k * ldb + 8 + 2 * t4);
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
+    for (int mi = 0; mi < MI; ++mi) {
       const double am = sgn * A[(8 * mi + g) * lda + k];
       c[mi][0][0] = fma(am, b0.x, c[mi][0][0]);
       c[mi][0][1] = fma(am, b0.y, c[mi][0][1]);
@@ -225,17 +237,16 @@ __device__ __forceinline__ void tile_32x16(const double* A, int lda, const doubl
   }
 }
 #else
-// one 32x16 DMMA tile: C (+)= sgn * A[32 x 32] * B[32 x 16]
-//   A element (m, k) at A + m*lda + k ; B element (k, n) at B + k*ldb + n
-__device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
-                                           double c[4][2][2], int lane, double sgn) {
+template <int MI, int KK>
+__device__ __forceinline__ void tile_mk(const double* A, int lda, const double* B, int ldb,
+                                        double c[4][2][2], int lane, double sgn) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int kk = 0; kk < 32; kk += 4) {
+  for (int kk = 0; kk < KK; kk += 4) {
     const double b0 = B[(kk + t4) * ldb + g];
     const double b1 = B[(kk + t4) * ldb + 8 + g];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) {
+    for (int mi = 0; mi < MI; ++mi) {
       const double am = sgn * A[(8 * mi + g) * lda + kk + t4];
       dmma(c[mi][0][0], c[mi][0][1], am, b0);
       dmma(c[mi][1][0], c[mi][1][1], am, b1);
@@ -243,12 +254,17 @@ __device__ __forceinline__ void tile_32x16(const double* A, int lda, const doubl
   }
 }
 #endif
+__device__ __forceinline__ void tile_32x16(const double* A, int lda, const double* B, int ldb,
+                                           double c[4][2][2], int lane, double sgn) {
+  tile_mk<4, 32>(A, lda, B, ldb, c, lane, sgn);
+}
 
-// C tile (32 x 16) at base (row stride lds) -> registers / back
+// C tile (8 MI x 16) at base (row stride lds) -> registers / back
+template <int MI = 4>
 __device__ __forceinline__ void load_c(const double* base, int lds, double c[4][2][2], int lane) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni) {
       const double2 v = *reinterpret_cast<const double2*>(base + (8 * mi + g) * lds + 8 * ni + 2 * t4);
@@ -256,10 +272,11 @@ __device__ __forceinline__ void load_c(const double* base, int lds, double c[4][
       c[mi][ni][1] = v.y;
     }
 }
+template <int MI = 4>
 __device__ __forceinline__ void store_c(double* base, int lds, const double c[4][2][2], int lane) {
   const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 2; ++ni)
       *reinterpret_cast<double2*>(base + (8 * mi + g) * lds + 8 * ni + 2 * t4) =
@@ -324,14 +341,21 @@ struct Rows {
   }
 };
 
-template <bool SPLIT>
+// HALF: NPB is an odd multiple of 16 (narrow-line instance only): the last
+// panel is 16 wide.  HALF = false compiles the 32-wide-panel code alone.
+template <bool SPLIT, bool HALF = false>
 __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, double off,
                                            const Rows<SPLIT> R, double* fac, int* bad, double* W0,
                                            double* W1, double* JL) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = BF_THREADS / 32;
   const int NPB = s.pad_, NPS = s.NPS, n = 2 * s.nc, nr = s.nr, lds = R.lds;
-  const int npan = NPB / 32, nct = NPB / 16;
+  // NPB is a multiple of 32, or (narrow lines, ocp_block_narrow.cu) of 16: the
+  // last panel is then 16 wide - one column tile, 16-row tiles, 16 pivot columns
+  const int npan = (NPB + 31) / 32, nct = NPB / 16;
+  auto pwid = [&](int p) { return HALF && p == npan - 1 ? 16 : 32; };
+  constexpr bool ALLP1 = LAW == BF_THREADS / 32;   // every warp is a pivot warp (needs the serial schedule)
+  static_assert(!ALLP1 || P1_SERIAL, "LAW == warps per CTA needs OCP_P1_SERIAL");
   const double off2 = off * off;
   const long long lsz = block_line_doubles(NPS);   // stored doubles per line
   BPH_START();
@@ -395,7 +419,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     // the other warps build the remaining rows (3 % faster than E for all
     // rows, then the first pivot inverse on 8 warps)
     const bool grpA = warp < LAW;
-    const int e_lo = grpA ? 0 : 32, e_hi = grpA ? 32 : NPB;
+    const int e_lo = grpA ? 0 : 32, e_hi = grpA && !ALLP1 && NPB > 32 ? 32 : NPB;
     const int e_w = grpA ? warp : warp - LAW, e_nw = grpA ? LAW : NW - LAW;
     // (rows wider than 256 columns are processed in chunks of 256)
     for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw)
@@ -454,7 +478,7 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     }
     if (grpA) {
       asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
-      pivot_inverse32<LAW>(R.row(0), lds, W0, W1, warp, lane, bad, pivot_kmax(n, 0));
+      pivot_inverse32<LAW>(R.row(0), lds, W0, W1, warp, lane, bad, pivot_kmax(n, 0), pwid(0));
     }
     __syncthreads();
     BPH_MARK(1);
@@ -475,12 +499,18 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
       double* Prow = R.row(p0);                 // the pivot row block
       const double* Pinv = Prow + p0;
       // ---- P2: row block S[p, j] = Pinv S[p, j] (column tiles of 16 outside p)
-      for (int tI = warp; tI < nct - 2; tI += NW) {
-        const int j0 = 16 * (tI + (tI >= 2 * p ? 2 : 0));
+      const int pw = pwid(p), pc = pw / 16;   // this panel's width and column tiles
+      for (int tI = warp; tI < nct - pc; tI += NW) {
+        const int j0 = 16 * (tI + (tI >= 2 * p ? pc : 0));
         if (j0 >= NPS) continue;   // identity padding: M[p, j] = 0 stays 0
         double c[4][2][2] = {};
-        tile_32x16(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
-        store_c(Prow + j0, lds, c, lane);
+        if (pw == 32) {
+          tile_mk<4, 32>(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
+          store_c<4>(Prow + j0, lds, c, lane);
+        } else {
+          tile_mk<2, 16>(Pinv, lds, Prow + j0, lds, c, lane, 1.0);
+          store_c<2>(Prow + j0, lds, c, lane);
+        }
       }
       __syncthreads();
       BPH_MARK(2);
@@ -491,17 +521,17 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
         auto upper = [&](int tI, int& rt, int& ct) {
           for (rt = 0; rt < npan; ++rt) {
             if (rt == p) continue;
-            const int cnt = nct - 2 * rt - (p > rt ? 2 : 0);
+            const int cnt = nct - 2 * rt - (p > rt ? pc : 0);
             if (tI < cnt) {
               ct = 2 * rt + tI;
-              if (p > rt && ct >= 2 * p) ct += 2;
+              if (p > rt && ct >= 2 * p) ct += pc;
               return true;
             }
             tI -= cnt;
           }
           return false;
         };
-        const int total = p * (nct - 2) - p * (p - 1) +
+        const int total = p * (nct - pc) - p * (p - 1) +
                           (npan - 1 - p) * nct - (npan - 1 - p) * (npan + p);
         const bool la = p + 1 < npan;
         const int g = lane >> 2, t4 = lane & 3;
@@ -511,10 +541,22 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           if (16 * ct >= NPS) return;   // padding columns: M[p, j] = 0, no update
           double* Ci = R.row(32 * rt);
           double c[4][2][2];
-          load_c(Ci + 16 * ct, lds, c, lane);
-          tile_32x16(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
-          store_c(Ci + 16 * ct, lds, c, lane);
+          const int rw = pwid(rt);   // rows of this row tile
+          if (rw == 32 && pw == 32) {
+            load_c<4>(Ci + 16 * ct, lds, c, lane);
+            tile_mk<4, 32>(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
+            store_c<4>(Ci + 16 * ct, lds, c, lane);
+          } else if (rw == 32) {
+            load_c<4>(Ci + 16 * ct, lds, c, lane);
+            tile_mk<4, 16>(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
+            store_c<4>(Ci + 16 * ct, lds, c, lane);
+          } else {   // (the half-width panel is the last one: the pivot panel is a full one)
+            load_c<2>(Ci + 16 * ct, lds, c, lane);
+            tile_mk<2, 32>(Ci + p0, lds, Prow + 16 * ct, lds, c, lane, -1.0);
+            store_c<2>(Ci + 16 * ct, lds, c, lane);
+          }
           if (ct >= 2 * rt + 2) {   // strictly upper: mirror into the lower triangle
+            // (a 16-row tile is never strictly upper: the half-width panel is the last one)
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -532,10 +574,11 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
         //      writes them as 16 contiguous entries of row 32rt + l.  It must
         //      follow every P3a tile (they read the old column block).
         auto p3b = [&](int rank, int nw) {   // rank: this warp's index among the nw doing it
-          for (int task = rank; task < 2 * (npan - 1); task += nw) {
-            int rt = task >> 1;
+          for (int task = rank; task < pc * (npan - 1); task += nw) {
+            int rt = task >> (pc - 1);   // pc is 1 or 2
+            const int c0 = 16 * (task - (rt << (pc - 1))), i = 32 * (rt + (rt >= p ? 1 : 0)) + lane;
             rt += rt >= p ? 1 : 0;
-            const int c0 = 16 * (task & 1), i = 32 * rt + lane;
+            if (i >= NPB) continue;   // (half-width last row tile)
             double v[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) v[c] = Prow[(c0 + c) * lds + i];
@@ -544,7 +587,8 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
             for (int c = 0; c < 16; c += 2)
               *reinterpret_cast<double2*>(dst + c) = make_double2(v[c], v[c + 1]);
           }
-          for (int e = 32 * rank + lane; e < 32 * 32; e += 32 * nw) {   // pivot block -> -A^{-1}
+          for (int e = 32 * rank + lane; e < 32 * pw; e += 32 * nw) {   // pivot block -> -A^{-1}
+            if ((e & 31) >= pw) continue;
             double* q = Prow + (e >> 5) * lds + p0 + (e & 31);
             *q = -*q;
           }
@@ -564,15 +608,20 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
           const bool law = warp < LAW;
           const int lrank = warp, trank = warp - LAW;
 #ifdef OCP_P1_SERIAL
-          // A/B: no overlap - every warp does trailing tiles, then warps
-          // 0..LAW-1 invert the next pivot block with the FP64 pipe to themselves
+          // no overlap (A/B on wide lines; the narrow-line instance, where
+          // every warp is a pivot warp): every warp does trailing tiles, then
+          // warps 0..LAW-1 invert the next pivot block with the FP64 pipe to
+          // themselves
           for (int tI = warp; tI < total; tI += NW) tile(tI);
           __syncthreads();
           BPH_MARK(3);
-          if (law) {
+          if (law)
             pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad,
-                                 pivot_kmax(n, p0 + 32));
-          } else {
+                                 pivot_kmax(n, p0 + 32), pwid(p + 1));
+          if (ALLP1) {
+            __syncthreads();
+            p3b(warp, NW);
+          } else if (!law) {
             p3b(trank, NW - LAW);
           }
           __syncthreads();
@@ -584,17 +633,17 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
 #ifdef OCP_PHASE_TIMING
             const long long tla = clock64();
 #endif
-            if (lrank < 2) tile(la0 + lrank);   // the two lookahead tiles
+            if (lrank < pwid(p + 1) / 16) tile(la0 + lrank);   // the lookahead tiles (next pivot block)
             asm volatile("bar.arrive 5, %0;" ::"n"(BF_THREADS) : "memory");
             asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
             pivot_inverse32<LAW>(R.row(p0 + 32) + p0 + 32, lds, W0, W1, lrank, lane, bad,
-                                 pivot_kmax(n, p0 + 32));
+                                 pivot_kmax(n, p0 + 32), pwid(p + 1));
 #ifdef OCP_PHASE_TIMING
             if (tid == 0) atomicAdd(&g_bphase[0], (unsigned long long)(clock64() - tla));
 #endif
           } else if (!P1_SERIAL) {
             for (int tI = trank; tI < total; tI += NW - LAW)
-              if (tI != la0 && tI != la0 + 1) tile(tI);
+              if (tI < la0 || tI >= la0 + pwid(p + 1) / 16) tile(tI);
             asm volatile("bar.sync 5, %0;" ::"n"(BF_THREADS) : "memory");
             p3b(trank, NW - LAW);
           }
@@ -647,6 +696,11 @@ k_block_factor(const SubInfo* subs, const int* list, int cnt, Phys P, const doub
     // their diagonals after the scratch rows of this CTA
     if (s.nc > BF_JL_POINTS) JL = gscratch + (long long)blockIdx.x * gs_stride + (long long)s.pad_ * lds;
     if (s.pad_ <= BF_SMEM_MAX_NPB) {
+#ifdef OCP_NARROW_INSTANCE
+      if (s.pad_ & 16)
+        factor_one<false, true>(s, JD, P.off, Rows<false>{sm, nullptr, s.pad_, lds}, fac, &bad, W0, W1, JL);
+      else
+#endif
       factor_one<false>(s, JD, P.off, Rows<false>{sm, nullptr, s.pad_, lds}, fac, &bad, W0, W1, JL);
     } else {
       const int r0 = (SMEM_S / lds) / 32 * 32;   // rows that fit in shared memory

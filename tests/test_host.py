@@ -207,3 +207,47 @@ def test_buffer_pools_retire_to_the_process_cache(monkeypatch):
     nat.empty_cache()
     assert nat._RETIRED.cached == 0
     assert sorted(freed) == sorted([0x3000, 0x4000, 0x1000 if got == 0x2000 else 0x2000])
+
+
+def test_retired_cache_give_never_blocks_on_its_own_lock():
+    """A garbage-collection finalizer can run inside _RetiredCache.take / give while the
+    thread holds the cache lock (Engine teardown -> release_all -> give): give must not
+    block (it deadlocked the GPU suite against itself); the parked buffer is filed by
+    the next caller."""
+    from paper_2411_00546_b200 import _native as nat
+    c = nat._RetiredCache(limit_bytes=1 << 20)
+    c.give(0x1000, 256)
+    assert c.take(256) == 0x1000 and c.take(256) is None
+    assert c.lock.acquire(blocking=False)       # "inside take()" on this thread
+    try:
+        c.give(0x2000, 512)                     # re-entrant give: returns at once
+    finally:
+        c.lock.release()
+    assert c.cached == 0 and c._pending == [(0x2000, 512)]
+    assert c.take(512) == 0x2000                # filed and handed out by the next take
+    assert c.cached == 0 and not c._pending
+
+
+def test_retired_cache_survives_finalizers_during_take():
+    """Finalizers that give buffers back run at arbitrary allocation points: force a
+    collection from inside the locked region of take() through a dict subclass."""
+    import gc
+    from paper_2411_00546_b200 import _native as nat
+    c = nat._RetiredCache(limit_bytes=1 << 20)
+
+    class Victim:
+        def __del__(self):
+            c.give(0x3000, 1024)
+
+    class Probe(dict):
+        def get(self, k, d=None):
+            v = Victim()
+            v.loop = v          # a cycle: only the collector frees it
+            del v
+            gc.collect()        # the finalizer runs here, with c.lock held by take()
+            return dict.get(self, k, d)
+
+    c.free = Probe()
+    assert c.take(2048) is None
+    c.free = dict(c.free)
+    assert c.take(1024) == 0x3000
