@@ -99,6 +99,10 @@ struct ocp_ctx {
   unsigned long long* d_gbad = nullptr;   // first nonfinite phi'/phi'' of the global Jacobian
   int h_cap = 0;
   cudaStream_t stream = nullptr;
+  // narrow-line factor: the few subdomains beyond its shared block run the
+  // 12-warp kernel on a second stream beside the many small ones
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // pinned host staging
   double* h_norm2 = nullptr;   // squared residual norms per subdomain (finish_residual)
   double* h_rpart = nullptr;   // pinned: per-CTA partials of the last residual
@@ -387,21 +391,32 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
   {
     // persistent CTAs take subdomains in list order: largest work first
     // (global-memory Schur blocks, then nr * NPB^3), so the tail is short
-    if (!ctx->d_flist) {   // list + the work counter of the persistent CTAs
-      CK(gmalloc(&ctx->d_flist, (ctx->I + 1) * sizeof(int)));
-      CK(cudaMallocHost(&ctx->h_flist, (ctx->I + 1) * sizeof(int)));
+    if (!ctx->d_flist) {   // lists + the work counters of the persistent CTAs
+      CK(gmalloc(&ctx->d_flist, (ctx->I + 2) * sizeof(int)));
+      CK(cudaMallocHost(&ctx->h_flist, (ctx->I + 2) * sizeof(int)));
     }
     CK(cudaStreamSynchronize(ctx->stream));   // h_flist may still feed a previous copy
     std::vector<int> ord(list);
+    const int smem_npb = ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB;
     auto cost = [&](int i) {
       const SubInfo& su = ctx->subs[i];
       const double c = (double)su.nr * su.pad_ * su.pad_ * su.pad_;
-      return su.pad_ > (ctx->bf_narrow ? narrow_factor_max_npb() : BF_SMEM_MAX_NPB) ? 4.0 * c : c;
+      return su.pad_ > smem_npb ? 4.0 * c : c;
     };
     std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return cost(x) > cost(y); });
-    for (int i = 0; i < cnt; ++i) ctx->h_flist[i] = ord[i];
-    ctx->h_flist[cnt] = 0;
-    CK(cudaMemcpyAsync(ctx->d_flist, ctx->h_flist, (cnt + 1) * sizeof(int), cudaMemcpyHostToDevice,
+    // narrow instance: [wide subdomains][counter][the others][counter]
+    int nwide = 0;
+    if (ctx->bf_narrow && ctx->mc_K <= 1) {
+      std::stable_partition(ord.begin(), ord.end(), [&](int i) { return ctx->subs[i].pad_ > smem_npb; });
+      while (nwide < cnt && ctx->subs[ord[nwide]].pad_ > smem_npb) ++nwide;
+    }
+    int* hl = ctx->h_flist;
+    for (int i = 0; i < nwide; ++i) hl[i] = ord[i];
+    const int off2 = nwide ? nwide + 1 : 0;   // second list (all of it when there is no wide one)
+    if (nwide) hl[nwide] = 0;
+    for (int i = nwide; i < cnt; ++i) hl[off2 + i - nwide] = ord[i];
+    hl[off2 + cnt - nwide] = 0;
+    CK(cudaMemcpyAsync(ctx->d_flist, hl, (cnt + (nwide ? 2 : 1)) * sizeof(int), cudaMemcpyHostToDevice,
                        ctx->stream));
     const int grid = std::min(cnt, ctx->bf_grid);
     if (ctx->mc_K > 1) {   // few wide subdomains: K CTAs each (status / barriers zeroed first)
@@ -418,8 +433,26 @@ int launch_factor(ocp_ctx* ctx, const int* d_list, const std::vector<int>& list,
       }
       CK(e);
     } else if (ctx->bf_narrow) {
-      CK(launch_narrow_factor(grid, ctx->stream, ctx->d_subs, ctx->d_flist, cnt, &ctx->P, ctx->JD,
-                              fac, ctx->bscratch, ctx->bs_stride, ctx->d_status));
+      if (nwide) {   // first, on the second stream: they take an SM each beside the narrow CTAs
+        if (!ctx->stream2) {
+          CK(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+          CK(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+          CK(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+        }
+        CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->stream2, ctx->ev_fork, 0));
+        k_block_factor<<<std::min(nwide, ctx->num_sms), block_factor_threads(),
+                         block_factor_smem_bytes(ctx->maxNPB), ctx->stream2>>>(
+            ctx->d_subs, ctx->d_flist, nwide, ctx->P, ctx->JD, fac, ctx->bscratch, ctx->bs_stride,
+            ctx->d_status);
+        CKL();
+        CK(cudaEventRecord(ctx->ev_join, ctx->stream2));
+      }
+      if (cnt > nwide)
+        CK(launch_narrow_factor(std::min(cnt - nwide, ctx->bf_grid), ctx->stream, ctx->d_subs,
+                                ctx->d_flist + off2, cnt - nwide, &ctx->P, ctx->JD, fac, ctx->bscratch,
+                                ctx->bs_stride, ctx->d_status));
+      if (nwide) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
     } else {
       k_block_factor<<<grid, block_factor_threads(), block_factor_smem_bytes(ctx->maxNPB),
                        ctx->stream>>>(ctx->d_subs, ctx->d_flist, cnt, ctx->P, ctx->JD, fac,
@@ -798,6 +831,9 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
   }
   for (auto e : ctx->free_events) cudaEventDestroy(e);
   for (auto e : ctx->marks) if (e) cudaEventDestroy(e);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->stream2) cudaStreamDestroy(ctx->stream2);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
