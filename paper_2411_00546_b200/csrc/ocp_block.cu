@@ -421,39 +421,47 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
     const bool grpA = warp < LAW;
     const int e_lo = grpA ? 0 : 32, e_hi = grpA && !ALLP1 && NPB > 32 ? 32 : NPB;
     const int e_w = grpA ? warp : warp - LAW, e_nw = grpA ? LAW : NW - LAW;
-    // (rows wider than 256 columns are processed in chunks of 256)
-    for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw)
+    // (rows wider than 256 columns are processed in chunks of 256; PACK - lines
+    // of at most 128 columns, the narrow instance - puts two row pairs in the
+    // four column slots of a lane, so twice the loads are in flight per warp)
+    constexpr bool PACK = HALF;
+    for (int i0 = e_lo + 2 * e_w; i0 < e_hi; i0 += 2 * e_nw * (PACK ? 2 : 1))
       for (int cb = 0; cb < NPB; cb += 256) {
         double2 v[2][4];
+        auto rowof = [&](int u) { return i0 + (PACK ? 2 * e_nw * (u >> 1) : 0); };   // first row of slot u's pair
+        auto colof = [&](int u) { return cb + 2 * lane + 64 * (PACK ? (u & 1) : u); };
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int j = cb + 2 * lane + 64 * u;
-            v[r][u] = (a > 0 && j < NPB) ? *reinterpret_cast<const double2*>(R.row(i0 + r) + j)
-                                         : make_double2(0.0, 0.0);
+            const int j = colof(u);
+            v[r][u] = (a > 0 && j < NPB && rowof(u) < e_hi)
+                          ? *reinterpret_cast<const double2*>(R.row(rowof(u) + r) + j)
+                          : make_double2(0.0, 0.0);
           }
         if (a > 0)
 #pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int i = i0 + r, m16 = 16 * (i >> 4) + 16;
-            if (i >= NPS) continue;
-            double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, NPS / 16) +
-                                                      (long long)(i & 15) * (m16 + 2));
+          for (int r = 0; r < 2; ++r)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int j = cb + 2 * lane + 64 * u;
-              if (j < m16) __stcs(col + (j >> 1), v[r][u]);
-            }
-          }
+              if (!PACK && u > 0) break;   // (one row pair: its column slots are handled below)
+              if (PACK && (u & 1)) continue;
+              const int i = rowof(u) + r, m16 = 16 * (i >> 4) + 16;
+              if (i >= NPS || rowof(u) >= e_hi) continue;
+              double2* col = reinterpret_cast<double2*>(dstl + block_col_off(i >> 4, NPS / 16) +
+                                                        (long long)(i & 15) * (m16 + 2));
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int i = i0 + r;
-          double* rw = R.row(i);
+              for (int u2 = 0; u2 < (PACK ? 2 : 4); ++u2) {
+                const int j = colof(u + u2);
+                if (j < m16) __stcs(col + (j >> 1), v[r][u + u2]);
+              }
+            }
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int j = cb + 2 * lane + 64 * u;
-            if (j >= NPB) continue;
+            const int i = rowof(u) + r, j = colof(u);
+            if (j >= NPB || rowof(u) >= e_hi) continue;
             double2 w;
             if (i < n && j < n) {
               w.x = off2 * v[1 - r][u].y;
@@ -462,9 +470,8 @@ __device__ __forceinline__ void factor_one(const SubInfo& s, const double* JD, d
               w.x = i == j ? 1.0 : 0.0;
               w.y = i == j + 1 ? 1.0 : 0.0;
             }
-            *reinterpret_cast<double2*>(rw + j) = w;
+            *reinterpret_cast<double2*>(R.row(i) + j) = w;
           }
-        }
       }
     if (grpA) asm volatile("bar.sync 2, %0;" ::"n"(32 * LAW) : "memory");
     else asm volatile("bar.sync 3, %0;" ::"n"(BF_THREADS - 32 * LAW) : "memory");
