@@ -513,7 +513,7 @@ def cpu_anchors(stress):
         if it:
             gpu_ms.append((time.perf_counter() - t0) * 1e3)
         release_local_systems(dec, fresh)
-    gpu_s = statistics.mean(gpu_ms) / 1e3
+    gpu_s = statistics.median(gpu_ms) / 1e3   # (median: a context teardown landing in one solve is an outlier)
     out["cfg2_whole_solve"] = {
         "workload": "BASELINE config 2 raspen_solve from x=0 (255^2, 4x4, overlap 8, inner tol 1e-8)",
         "cpu_s": cpu_s, "gpu_e2e_s": gpu_s, "speedup": cpu_s / gpu_s,

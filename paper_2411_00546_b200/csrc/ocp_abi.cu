@@ -770,8 +770,9 @@ int ocp_ctx_create(int n, int s1, int s2, int overlap, double nu, double mu, int
   ctx->h_cap = 4096;
   CKC(gmalloc(&ctx->d_h, ctx->h_cap * sizeof(double)));
   CKC(cudaMallocHost(&ctx->h_norm2, I * sizeof(double)));
-  CKC(cudaMallocHost(&ctx->h_rpart, (size_t)I * ctx->res_chunks * sizeof(double)));
-  CKC(cudaMallocHost(&ctx->h_rbad, (size_t)I * ctx->res_chunks * sizeof(unsigned long long)));
+  // (one pinned allocation for both: cudaMallocHost / cudaFreeHost cost milliseconds)
+  CKC(cudaMallocHost(&ctx->h_rpart, 2 * (size_t)I * ctx->res_chunks * sizeof(double)));
+  ctx->h_rbad = reinterpret_cast<unsigned long long*>(ctx->h_rpart + (size_t)I * ctx->res_chunks);
   ctx->res_bad.assign(I, -1ll);
   CKC(cudaMallocHost(&ctx->h_status, I * sizeof(int)));
   CKC(cudaMallocHost(&ctx->h_bad, I * sizeof(long long)));
@@ -820,7 +821,7 @@ void ocp_ctx_destroy(ocp_ctx* ctx) {
                   (void*)ctx->d_gbad, (void*)ctx->bscratch, (void*)ctx->d_flist, (void*)ctx->d_solve_order,
                   (void*)ctx->d_h})
     if (p) gfree(p);
-  for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_rpart, (void*)ctx->h_rbad, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
+  for (void* p : {(void*)ctx->h_norm2, (void*)ctx->h_rpart, (void*)ctx->h_status, (void*)ctx->h_bad, (void*)ctx->h_list,
                   (void*)ctx->h_alpha, (void*)ctx->h_small, (void*)ctx->h_flags,
                   (void*)ctx->gm_hh, (void*)ctx->st_hhist, (void*)ctx->h_flist})
     if (p) cudaFreeHost(p);
