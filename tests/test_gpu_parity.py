@@ -296,6 +296,34 @@ def test_cfg5_sweep_and_jvp_match_reference(name):
         assert abs(np.linalg.norm(vec) - float(g[f"{key}_norm"])) <= 1e-10 * float(g[f"{key}_norm"])
 
 
+@pytest.mark.parametrize("n,parts,m", [(400, 20, 2), (360, 18, 4), (320, 20, 2), (395, 18, 3)])
+def test_many_small_subdomains_sweep_and_jvp_match_oracle(n, parts, m):
+    """Decompositions of >= 2 subdomains per SM run the narrow-line factor instance
+    (ocp_block_narrow.cu): lines padded to 16 with a half-width last panel (local sides
+    24 / 28 -> 48 / 56 unknowns at NPB = 48 / 64, uneven tilings with larger last tiles
+    that go to the 12-warp kernel on the second stream), lines that are a multiple of 32
+    (54 unknowns at NPB = 64), and an 82-unknown corner (n = 395: 17 tiles of 21 and one of 38)
+    beyond the instance (12-warp kernel, second stream).  One RAS sweep at fixed
+    eps and one JVP against the oracle's SuperLU path (schwarz.py:285-345)."""
+    from paper_2411_00546_b200.schwarz import _jvp, _sweep
+    phi, nu, mu, eps = make_phi("cubic"), 1e-3, 1e-2, 1e-3
+    spec = unit_spec(n, phi, nu, mu)
+    dec = decompose(spec.grid, parts, parts, m)
+    assert len(dec.subdomains) >= 296
+    eng = build_local_systems(dec, spec)
+    prob = O.Problem(n, parts, parts, m, phi, nu, mu, spec.f, spec.y_d)
+    x0 = np.zeros(2 * n * n)
+    x = eng.from_host(x0)
+    fac = eng.factor_store()
+    fval, inner = _sweep(eng, x, fac, ContinuationSchedule.fixed(eps), NewtonConfig(tol=1e-8, max_outer=200))
+    f_ref, corr = O.raspen_residual(prob, x0, eps, tol=1e-8, threads=8)
+    assert inner == corr.inner
+    assert rel_l2(fval.to_host(), f_ref) <= 1e-10
+    d = np.random.default_rng(5).standard_normal(2 * n * n)
+    out = _jvp(eng, fac, eng.from_host(d)).to_host()
+    assert rel_l2(out, O.raspen_jvp(prob, x0, d, eps, corr)) <= 1e-10
+
+
 def test_jvp_properties_linear_zero_and_single_domain_identity():
     """Reference property tests (`test_schwarz.py:285-308`) on the device path."""
     tag, n, s1, s2, m, phi, nu, mu = UNIT_CASES[0]
