@@ -296,7 +296,7 @@ def test_cfg5_sweep_and_jvp_match_reference(name):
         assert abs(np.linalg.norm(vec) - float(g[f"{key}_norm"])) <= 1e-10 * float(g[f"{key}_norm"])
 
 
-@pytest.mark.parametrize("n,parts,m", [(400, 20, 2), (360, 18, 4), (320, 20, 2), (395, 18, 3)])
+@pytest.mark.parametrize("n,parts,m", [(400, 20, 2), (360, 18, 4), (320, 20, 2), (395, 18, 3), (60, 20, 1)])
 def test_many_small_subdomains_sweep_and_jvp_match_oracle(n, parts, m):
     """Decompositions of >= 2 subdomains per SM run the narrow-line factor instance
     (ocp_block_narrow.cu): lines padded to 16 with a half-width last panel (local sides
