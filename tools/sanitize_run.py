@@ -2,7 +2,7 @@
 racecheck / synccheck, one tool per process):
 
 * RASPEN solve on the cubic20 unit case and BASELINE config 1 - local
-  residual (tickets), batched block factor (12-warp and narrow instances),
+  residual (per-CTA partials), batched block factor (12-warp and narrow instances),
   block solve (mbarrier TMA ring, named barriers), fused JVP, cooperative
   lagged-dot Arnoldi (atomic grid barrier), scatter / vector kernels;
 * newton-ras-eps on config 1 - global residual / Jacobian / JVP, RAS apply;
